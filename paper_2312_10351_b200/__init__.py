@@ -1,0 +1,34 @@
+"""paper_2312_10351_b200 — Opara's operator-parallel DAG executor, B200-native.
+
+Drop-in for the reference ``opsched`` package's hot path: the same public
+names for the graph model, the stream allocator (Alg. 1) and the launch
+orderer (Alg. 2), computed by the C++ scheduler in libopara.so; and, in place
+of the reference's simulated "run", a real multi-stream CUDA Graph executor
+with hand-written sm_100a kernels (``compile`` / ``ScheduledGraph.run``).
+"""
+
+__version__ = "0.1.0"
+
+from .dag import (ComputationGraph, OpClass, OperatorNode, ResourceDemand, apply_profile,
+                  classify, graph_from_dict, graph_to_dict, load_graph, save_graph)
+from .device import (DEFAULT_GPU, GPU_PRESETS, GpuConfig, device_gpu_config, gpu_config_to_dict,
+                     load_gpu_config)
+from .errors import (CoverageError, CudaError, FormatError, GraphValidationError,
+                     InfeasibleBlockError, PlanViolationError, SchedulerError)
+from .order import (POLICIES, LaunchSchedule, ResourceScore, dominant_share, load_schedule,
+                    make_order, order_baseline, order_opara, resource_score, save_schedule,
+                    schedule_to_dict)
+from .plan import (DEFAULT_SYNC_OVERHEAD_US, PlanCost, StreamPlan, allocate_streams, load_plan,
+                   plan_to_dict, save_plan, single_stream_plan, validate_plan)
+
+__all__ = [
+    "__version__", "ComputationGraph", "CoverageError", "CudaError", "DEFAULT_GPU",
+    "DEFAULT_SYNC_OVERHEAD_US", "FormatError", "GPU_PRESETS", "GpuConfig", "GraphValidationError",
+    "InfeasibleBlockError", "LaunchSchedule", "OpClass", "OperatorNode", "POLICIES", "PlanCost",
+    "PlanViolationError", "ResourceDemand", "ResourceScore", "SchedulerError", "StreamPlan",
+    "allocate_streams", "apply_profile", "classify", "device_gpu_config", "dominant_share",
+    "gpu_config_to_dict", "graph_from_dict", "graph_to_dict", "load_gpu_config", "load_graph",
+    "load_plan", "load_schedule", "make_order", "order_baseline", "order_opara", "plan_to_dict",
+    "resource_score", "save_graph", "save_plan", "save_schedule", "schedule_to_dict",
+    "single_stream_plan", "validate_plan",
+]

@@ -1,0 +1,58 @@
+// Operator registry shared by the executor and the kernel families.
+//
+// Parameter layout of opara_op per kind (all shapes NHWC, batch-major; a
+// "channel view" is (buffer, cstride, coff): element (pixel q, channel c)
+// lives at buffer[q * cstride + coff + c], which is how concat is eliminated —
+// producers store straight into their slice of the concatenated buffer).
+//
+// CONV2D       i: 0 N, 1 H, 2 W, 3 Cin, 4 in_cstride, 5 in_coff,
+//                 6 OH, 7 OW, 8 Cout, 9 out_cstride, 10 out_coff,
+//                 11 R, 12 S, 13 stride_h, 14 stride_w, 15 pad_h, 16 pad_w,
+//                 17 relu, 18 dtype (0 f32), 19 split_k (1)
+//              p: 0 in, 1 weight [R*S*Cin][Cout] (k = (r*S + s)*Cin + c), 2 bias [Cout], 3 out
+//              variant: tile id (conv.cu)
+// MAXPOOL2D /  i: 0 N, 1 H, 2 W, 3 C, 4 in_cstride, 5 in_coff, 6 OH, 7 OW, 8 out_cstride,
+// AVGPOOL2D       9 out_coff, 10 kh, 11 kw, 12 sh, 13 sw, 14 ph, 15 pw,
+//                 16 count_include_pad (avg), 18 dtype
+//              p: 0 in, 3 out
+// GLOBAL_AVGPOOL i: 0 N, 1 H, 2 W, 3 C, 4 in_cstride, 5 in_coff, 18 dtype;  p: 0 in, 3 out [N][C]
+// LINEAR       i: 0 M (rows), 1 K, 2 N (out features), 3 act (0 none, 1 relu, 2 gelu, 3 tanh),
+//                 4 x_stride, 5 y_stride, 18 dtype
+//              p: 0 x [M][K], 1 W [N][K], 2 bias [N] (nullable), 3 y [M][N]
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "opara.h"
+
+namespace opara {
+
+struct LaunchCfg {
+  const void* func = nullptr;
+  dim3 grid{1, 1, 1};
+  dim3 block{1, 1, 1};
+  size_t smem = 0;
+};
+
+// trace: nullable device pointer to two u64 slots (min start, max end ns).
+// dry: only fill `cfg` (no device access), used for profiles on CPU hosts.
+using Launcher = opara_status (*)(const opara_op& op, cudaStream_t s, unsigned long long* trace,
+                                  LaunchCfg* cfg, bool dry);
+
+opara_status launch_conv2d(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+opara_status launch_pool2d(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+opara_status launch_global_avgpool(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*,
+                                   bool);
+opara_status launch_linear(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+
+// Dispatch on op.kind.
+opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* trace,
+                       LaunchCfg* cfg, bool dry);
+
+opara_status cuda_fail(cudaError_t e, const char* what);
+
+inline unsigned ceil_div(int64_t a, int64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+}  // namespace opara

@@ -1,0 +1,187 @@
+// NHWC pooling kernels (memory-bound).  One thread per (output pixel, 4
+// channels): 128-bit loads/stores when the channel view is 16-byte aligned,
+// scalar otherwise.  Grid-stride loops with a bounded grid.
+
+#include "device_common.cuh"
+#include "ops.h"
+#include "status.h"
+
+namespace opara {
+namespace {
+
+struct PoolArgs {
+  const float* __restrict__ in;
+  float* __restrict__ out;
+  int N, H, W, C, in_cs, in_coff;
+  int OH, OW, out_cs, out_coff;
+  int kh, kw, sh, sw, ph, pw;
+  int include_pad;
+};
+
+// Window semantics follow torch's pooling (max: padding never wins; avg:
+// divisor counts padded cells when count_include_pad, clipped at H+pad).
+template <bool kMax, int V>
+__global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long long* trace) {
+  trace_begin(trace);
+  const int cv = a.C / V;
+  const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(idx % cv) * V;
+    const int64_t q = idx / cv;
+    const int ow = static_cast<int>(q % a.OW);
+    const int oh = static_cast<int>((q / a.OW) % a.OH);
+    const int b = static_cast<int>(q / (static_cast<int64_t>(a.OW) * a.OH));
+    int hs = oh * a.sh - a.ph, ws = ow * a.sw - a.pw;
+    int he = min(hs + a.kh, a.H + a.ph), we = min(ws + a.kw, a.W + a.pw);
+    const int pool_size = (he - hs) * (we - ws);
+    hs = max(hs, 0);
+    ws = max(ws, 0);
+    he = min(he, a.H);
+    we = min(we, a.W);
+    float acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = kMax ? -INFINITY : 0.f;
+    for (int ih = hs; ih < he; ++ih) {
+      for (int iw = ws; iw < we; ++iw) {
+        const float* src = a.in + (static_cast<int64_t>(b * a.H + ih) * a.W + iw) * a.in_cs + a.in_coff + c;
+        float x[V];
+        if constexpr (V == 4) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(src));
+          x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) x[v] = __ldg(src + v);
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if constexpr (kMax) {
+            // NaN propagates like torch (x > acc || isnan(x))
+            acc[v] = (x[v] > acc[v] || isnan(x[v])) ? x[v] : acc[v];
+          } else {
+            acc[v] += x[v];
+          }
+        }
+      }
+    }
+    if constexpr (!kMax) {
+      const int div = a.include_pad ? pool_size : (he - hs) * (we - ws);
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] = acc[v] / static_cast<float>(div);
+    }
+    float* dst = a.out + q * a.out_cs + a.out_coff + c;
+    if constexpr (V == 4) {
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) dst[v] = acc[v];
+    }
+  }
+  trace_end(trace);
+}
+
+// Global average pool: one warp per (batch, 4-channel group) when C is large;
+// the warp strides over the H*W pixels and shuffles the partial sums.
+__global__ void __launch_bounds__(256) global_avgpool_nhwc(const float* __restrict__ in,
+                                                           float* __restrict__ out, int N, int HW,
+                                                           int C, int in_cs, int in_coff,
+                                                           unsigned long long* trace) {
+  trace_begin(trace);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  const int64_t total = static_cast<int64_t>(N) * C;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32; w < total;
+       w += warps) {
+    const int c = static_cast<int>(w % C);
+    const int b = static_cast<int>(w / C);
+    float s = 0.f;
+    for (int p = lane; p < HW; p += 32)
+      s += __ldg(in + (static_cast<int64_t>(b) * HW + p) * in_cs + in_coff + c);
+    s = warp_sum(s);
+    if (lane == 0) out[static_cast<int64_t>(b) * C + c] = s / static_cast<float>(HW);
+  }
+  trace_end(trace);
+}
+
+// Small-HW variant: one thread per channel, sequential over pixels; coalesced
+// across channels (the common 7x7 / 8x8 tail of CNNs).
+__global__ void __launch_bounds__(128) global_avgpool_nhwc_cols(const float* __restrict__ in,
+                                                                float* __restrict__ out, int N,
+                                                                int HW, int C, int in_cs,
+                                                                int in_coff,
+                                                                unsigned long long* trace) {
+  trace_begin(trace);
+  const int64_t total = static_cast<int64_t>(N) * C;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(t % C);
+    const int b = static_cast<int>(t / C);
+    const float* src = in + static_cast<int64_t>(b) * HW * in_cs + in_coff + c;
+    float s = 0.f;
+    for (int p = 0; p < HW; ++p) s += __ldg(src + static_cast<int64_t>(p) * in_cs);
+    out[t] = s / static_cast<float>(HW);
+  }
+  trace_end(trace);
+}
+
+}  // namespace
+
+opara_status launch_pool2d(const opara_op& op, cudaStream_t s, unsigned long long* trace,
+                           LaunchCfg* cfg, bool dry) {
+  PoolArgs a;
+  a.in = static_cast<const float*>(op.p[0]);
+  a.out = static_cast<float*>(op.p[3]);
+  a.N = (int)op.i[0]; a.H = (int)op.i[1]; a.W = (int)op.i[2]; a.C = (int)op.i[3];
+  a.in_cs = (int)op.i[4]; a.in_coff = (int)op.i[5];
+  a.OH = (int)op.i[6]; a.OW = (int)op.i[7]; a.out_cs = (int)op.i[8]; a.out_coff = (int)op.i[9];
+  a.kh = (int)op.i[10]; a.kw = (int)op.i[11]; a.sh = (int)op.i[12]; a.sw = (int)op.i[13];
+  a.ph = (int)op.i[14]; a.pw = (int)op.i[15]; a.include_pad = (int)op.i[16];
+  if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "pool2d: fp32 only");
+  const bool is_max = op.kind == OPARA_OP_MAXPOOL2D;
+  const bool vec = (a.C % 4 == 0) && (a.in_cs % 4 == 0) && (a.in_coff % 4 == 0) &&
+                   (a.out_cs % 4 == 0) && (a.out_coff % 4 == 0) &&
+                   (reinterpret_cast<uintptr_t>(a.in) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(a.out) % 16 == 0);
+  const int V = vec ? 4 : 1;
+  const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
+  LaunchCfg c;
+  if (is_max)
+    c.func = vec ? reinterpret_cast<const void*>(&pool2d_nhwc<true, 4>)
+                 : reinterpret_cast<const void*>(&pool2d_nhwc<true, 1>);
+  else
+    c.func = vec ? reinterpret_cast<const void*>(&pool2d_nhwc<false, 4>)
+                 : reinterpret_cast<const void*>(&pool2d_nhwc<false, 1>);
+  c.block = dim3(256);
+  c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(work, 256), 148u * 4u)));
+  if (cfg) *cfg = c;
+  if (dry) return OPARA_OK;
+  void* args[] = {&a, &trace};
+  return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, 0, s), "pool2d launch");
+}
+
+opara_status launch_global_avgpool(const opara_op& op, cudaStream_t s, unsigned long long* trace,
+                                   LaunchCfg* cfg, bool dry) {
+  const float* in = static_cast<const float*>(op.p[0]);
+  float* out = static_cast<float*>(op.p[3]);
+  int N = (int)op.i[0], H = (int)op.i[1], W = (int)op.i[2], C = (int)op.i[3];
+  int in_cs = (int)op.i[4], in_coff = (int)op.i[5];
+  if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "global_avgpool: fp32 only");
+  int HW = H * W;
+  LaunchCfg c;
+  const int64_t total = static_cast<int64_t>(N) * C;
+  if (HW <= 128) {
+    c.func = reinterpret_cast<const void*>(&global_avgpool_nhwc_cols);
+    c.block = dim3(128);
+    c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(total, 128), 148u * 4u)));
+  } else {
+    c.func = reinterpret_cast<const void*>(&global_avgpool_nhwc);
+    c.block = dim3(256);
+    c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(total, 8), 148u * 4u)));
+  }
+  if (cfg) *cfg = c;
+  if (dry) return OPARA_OK;
+  void* args[] = {&in, &out, &N, &HW, &C, &in_cs, &in_coff, &trace};
+  return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, 0, s), "global_avgpool launch");
+}
+
+}  // namespace opara

@@ -1,0 +1,60 @@
+"""Assemble a throw-away ``opsched`` package whose hot path is OURS.
+
+The reference test suite (/root/reference/pkg/tests, 158 tests) imports
+``opsched``.  This shim answers those imports with:
+
+* errors / graph / allocator / orderer  ->  paper_2312_10351_b200 (C++ via the C ABI)
+* simulator / oracle / generators / cli / __init__ / __main__  ->  the reference
+  modules themselves (symlinked into a temp dir, never copied into the repo);
+  they are out of the hot path and are the consumers of our outputs.
+
+Used only by tests/test_reference_suite.py in the build container (where
+/root/reference exists).
+"""
+
+from __future__ import annotations
+
+import os
+from pathlib import Path
+
+REF_SRC = Path("/root/reference/pkg/src/opsched")
+
+ERRORS = "from paper_2312_10351_b200.errors import *  # noqa\n" \
+         "from paper_2312_10351_b200.errors import (SchedulerError, FormatError, GraphValidationError,\n" \
+         "    PlanViolationError, CoverageError, InfeasibleBlockError)\n"
+GRAPH = "from paper_2312_10351_b200.dag import (OpClass, classify, ResourceDemand, OperatorNode,\n" \
+        "    ComputationGraph, load_graph, save_graph, graph_to_dict, apply_profile, _read_json)\n"
+ALLOCATOR = '''from paper_2312_10351_b200.plan import (DEFAULT_SYNC_OVERHEAD_US, PlanCost, StreamPlan,
+    allocate_streams, load_plan, plan_to_dict, save_plan, single_stream_plan, validate_plan,
+    plan_cost, require_valid)
+
+
+def evaluate_plan(g, plan, order, cfg, sync_overhead_us=DEFAULT_SYNC_OVERHEAD_US):
+    """Glue: our validation + plan_cost around the reference's simulated makespans."""
+    from .simulator import sequential_makespan_ns, simulate
+    require_valid(g, plan)
+    seq_ns = sequential_makespan_ns(g, cfg)
+    para_ns = simulate(g, plan, order, cfg).makespan_ns
+    cost = plan_cost(seq_ns / 1000, para_ns / 1000, len(plan.sync_events), sync_overhead_us)
+    return PlanCost(cost.sequential_us, cost.parallel_us,
+                    para_ns / seq_ns if seq_ns else 0.0, cost.sync_count,
+                    cost.sync_overhead_us, cost.total_us, para_ns > seq_ns)
+'''
+ORDERER = "from paper_2312_10351_b200.order import (POLICIES, LaunchSchedule, ResourceScore,\n" \
+          "    dominant_share, resource_score, order_opara, order_baseline, make_order,\n" \
+          "    schedule_to_dict, save_schedule, load_schedule)\n" \
+          "from .simulator import GpuConfig  # noqa: F401\n"
+
+
+def make_shim(root: Path) -> Path:
+    pkg = root / "opsched"
+    pkg.mkdir(parents=True, exist_ok=True)
+    (pkg / "errors.py").write_text(ERRORS)
+    (pkg / "graph.py").write_text(GRAPH)
+    (pkg / "allocator.py").write_text(ALLOCATOR)
+    (pkg / "orderer.py").write_text(ORDERER)
+    for name in ("__init__.py", "__main__.py", "simulator.py", "oracle.py", "generators.py", "cli.py"):
+        link = pkg / name
+        if not link.exists():
+            os.symlink(REF_SRC / name, link)
+    return root
