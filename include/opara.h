@@ -141,7 +141,9 @@ opara_status opara_order(const opara_dag* dag, int32_t policy, const opara_gpu_c
 /* Operator kinds understood by the executor.  Parameter layout per kind is
  * documented in paper_2312_10351_b200/csrc/ops.h (struct opara_op.i[]). */
 typedef enum opara_op_kind {
-  OPARA_OP_CONV2D = 1,      /* NHWC implicit-GEMM conv + folded BN bias + ReLU, slice store */
+  OPARA_OP_NOP = 0,         /* join point without a kernel (eliminated concat):
+                               capture only applies its waits and records      */
+  OPARA_OP_CONV2D = 1,     /* NHWC implicit-GEMM conv + folded BN bias + ReLU, slice store */
   OPARA_OP_MAXPOOL2D = 2,   /* NHWC window max (ceil_mode aware)                          */
   OPARA_OP_AVGPOOL2D = 3,   /* NHWC window mean (count_include_pad aware)                 */
   OPARA_OP_GLOBAL_AVGPOOL = 4,

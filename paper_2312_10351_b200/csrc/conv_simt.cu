@@ -26,6 +26,8 @@ struct ConvArgs {
   int R, S, sh, sw, ph, pw;
   int relu;
   int M, K;
+  // input element (b, ih, iw, c) lives at in[b*sN + ih*sH + iw*sW + c*sC + in_coff]
+  int64_t sN, sH, sW, sC;
 };
 
 constexpr int BK = 16;
@@ -56,7 +58,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     if (m < a.M) {
       const int b = m / ohw, rem = m - b * ohw;
       const int oh = rem / a.OW, ow = rem - oh * a.OW;
-      a_base[j] = b * a.H;
+      a_base[j] = b;
       a_ih0[j] = oh * a.sh - a.ph;
       a_iw0[j] = ow * a.sw - a.pw;
     } else {
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
       const int ih = a_ih0[j] + r, iw = a_iw0[j] + s;
       float v = 0.f;
       if (kin && a_base[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W)
-        v = __ldg(a.in + (static_cast<int64_t>(a_base[j] + ih) * a.W + iw) * a.in_cs + a.in_coff + c);
+        v = __ldg(a.in + a_base[j] * a.sN + ih * a.sH + iw * a.sW + c * a.sC + a.in_coff);
       ra[j] = v;
     }
 #pragma unroll
@@ -205,6 +207,18 @@ opara_status launch_conv2d(const opara_op& op, cudaStream_t s, unsigned long lon
   if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "conv2d simt engine: fp32 only");
   a.M = a.N * a.OH * a.OW;
   a.K = a.R * a.S * a.Cin;
+  if (op.i[20]) {  // dense NCHW input
+    a.sC = static_cast<int64_t>(a.H) * a.W;
+    a.sW = 1;
+    a.sH = a.W;
+    a.sN = a.sC * a.Cin;
+    a.in_coff = 0;
+  } else {
+    a.sC = 1;
+    a.sW = a.in_cs;
+    a.sH = static_cast<int64_t>(a.W) * a.in_cs;
+    a.sN = a.sH * a.H;
+  }
   if (a.M <= 0 || a.Cout <= 0 || a.K <= 0) return fail(OPARA_ERR_VALUE, "conv2d: empty shape");
   int count = 0;
   const Variant* v = variants(&count);

@@ -31,6 +31,9 @@ opara_status cuda_fail(cudaError_t e, const char* what) {
 opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* trace,
                        LaunchCfg* cfg, bool dry) {
   switch (op.kind) {
+    case OPARA_OP_NOP:
+      if (cfg) *cfg = LaunchCfg{};
+      return OPARA_OK;
     case OPARA_OP_CONV2D: return launch_conv2d(op, s, trace, cfg, dry);
     case OPARA_OP_MAXPOOL2D:
     case OPARA_OP_AVGPOOL2D: return launch_pool2d(op, s, trace, cfg, dry);
@@ -300,7 +303,7 @@ opara_status opara_op_launch_config(const opara_op* op, opara_op_profile* out) {
   out->registers_per_thread = 0;
   out->isolated_us = 0.0;
   int count = 0;
-  if (cudaGetDeviceCount(&count) == cudaSuccess && count > 0) {
+  if (c.func && cudaGetDeviceCount(&count) == cudaSuccess && count > 0) {
     cudaFuncAttributes attr;
     if (cudaFuncGetAttributes(&attr, c.func) == cudaSuccess) {
       out->registers_per_thread = attr.numRegs;
@@ -325,6 +328,10 @@ opara_status opara_exec_profile(opara_exec* ex, int32_t reps, opara_op_profile* 
     opara::LaunchCfg c;
     st = opara::launch_op(ex->ops[i], s, nullptr, &c, true);
     if (st != OPARA_OK) break;
+    if (!c.func) {  // NOP join: no kernel, no demand
+      out[i] = opara_op_profile{1, 0, 0, 0, 0.0};
+      continue;
+    }
     cudaFuncAttributes attr;
     if (cudaFuncGetAttributes(&attr, c.func) != cudaSuccess) {
       st = fail(OPARA_ERR_CUDA, "cudaFuncGetAttributes failed");
@@ -432,7 +439,9 @@ opara_status opara_exec_time(opara_exec* ex, int32_t slot, int32_t warmup, int32
 
 int64_t opara_exec_num_launches(const opara_exec* ex, int32_t slot) {
   if (!ex || !ex->plans.count(slot)) return 0;
-  return static_cast<int64_t>(ex->ops.size());
+  int64_t n = 0;
+  for (const auto& op : ex->ops) n += op.kind != OPARA_OP_NOP;
+  return n;
 }
 
 opara_status opara_device_gpu_config(int32_t device, opara_gpu_config* out) {

@@ -1,0 +1,310 @@
+"""compile(model) -> ScheduledGraph: the "model in, scheduled graph out, run" entry.
+
+Pipeline ("B200 call stack"):
+
+1. lower the model (frontend.lower) to executor operators;
+2. place every buffer in HBM once (PyTorch allocates; nothing is freed or
+   re-used, so no write-after-read hazards exist between concurrent branches);
+3. create the libopara executor and profile every op alone (grid, block,
+   registers, shared memory, in-graph time) -> ResourceDemand per node;
+4. build the profiled DAG in C++, run Alg. 1 + Alg. 2 (or any baseline
+   policy) against the live device's GpuConfig;
+5. capture the multi-stream CUDA Graph of (plan, order) and, for reference,
+   the sequential single-stream CUDA Graph of the same kernels.
+
+``run`` is then one cudaGraphLaunch: the host crosses into the device once
+per inference.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+import os
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _lib
+from .dag import ComputationGraph, OperatorNode, ResourceDemand, graph_to_dict
+from .device import GpuConfig, device_gpu_config, GPU_PRESETS
+from .frontend import (AVGPOOL2D, CONV2D, GLOBAL_AVGPOOL, LINEAR, MAXPOOL2D, NOP, Program, lower)
+from .order import LaunchSchedule, make_order
+from .plan import StreamPlan, allocate_streams, plan_to_dict, single_stream_plan
+
+SLOT_PARALLEL = 0
+SLOT_SEQUENTIAL = 1
+
+
+def _device_fit(d: ResourceDemand, cfg: GpuConfig) -> int:
+    per_sm = cfg.max_blocks_per_sm
+    if d.threads_per_block:
+        per_sm = min(per_sm, cfg.threads_per_sm // d.threads_per_block)
+    if d.shared_mem_per_block:
+        per_sm = min(per_sm, cfg.shared_mem_per_sm // d.shared_mem_per_block)
+    if d.registers_per_block:
+        per_sm = min(per_sm, cfg.registers_per_sm // d.registers_per_block)
+    return max(1, per_sm) * cfg.num_sms
+
+
+def block_duration_us(isolated_us: float, d: ResourceDemand, cfg: GpuConfig) -> float:
+    """Per-block time under the reference's wave semantics: an op alone runs
+    ceil(blocks / device_fit) waves of one block duration (helpers.py:99-117)."""
+    waves = math.ceil(d.num_blocks / _device_fit(d, cfg))
+    return max(isolated_us / waves, 0.001)
+
+
+def _op_record(op, views, weights) -> _lib.OparaOp:
+    """Fill the POD launch record of one lowered op (layouts: csrc/ops.h)."""
+    rec = _lib.OparaOp()
+    rec.kind = op.kind
+    rec.variant = -1
+    if op.kind == NOP:
+        return rec
+    q = op.ints
+    (ib, icoff, ics, inchw), (ob, ocoff, ocs) = views
+    i = rec.i
+    if op.kind == CONV2D:
+        vals = [q["N"], q["H"], q["W"], q["Cin"], ics, icoff, q["OH"], q["OW"], q["Cout"], ocs, ocoff,
+                q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], 0, 1, int(inchw)]
+        rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
+    elif op.kind in (MAXPOOL2D, AVGPOOL2D):
+        vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff, q["OH"], q["OW"], ocs, ocoff, q["kh"],
+                q["kw"], q["sh"], q["sw"], q["ph"], q["pw"], q["include_pad"], 0, 0]
+        rec.p[0], rec.p[3] = ib, ob
+    elif op.kind == GLOBAL_AVGPOOL:
+        vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff] + [0] * 12 + [0]
+        rec.p[0], rec.p[3] = ib, ob
+    elif op.kind == LINEAR:
+        vals = [q["M"], q["K"], q["N"], q["act"], q["K"], q["N"]] + [0] * 12 + [0]
+        rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
+    else:
+        raise ValueError(f"unknown op kind {op.kind}")
+    for k, v in enumerate(vals):
+        i[k] = int(v)
+    return rec
+
+
+@dataclass
+class Timing:
+    median_ms: float
+    mean_ms: float
+    min_ms: float
+    samples: list
+
+
+class ScheduledGraph:
+    """A compiled model: profiled DAG, Opara plan + order, captured graphs."""
+
+    def __init__(self, program: Program, device: int, policy: str = "opara",
+                 gpu_config: GpuConfig | None = None, profile_reps: int = 20, seed: int | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("ScheduledGraph needs a CUDA device (there is no CPU fallback)")
+        self.program = program
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        self._bufs: dict[int, torch.Tensor] = {}
+        self._keep: list[torch.Tensor] = []
+        self._alloc(program)
+        recs = (_lib.OparaOp * len(program.ops))()
+        for k, op in enumerate(program.ops):
+            recs[k] = _op_record(op, self._views(op), self._weights(op))
+        self._recs = recs
+        L = _lib.lib()
+        h = C.c_void_p()
+        _lib.check(L.opara_exec_create(device, C.cast(recs, C.c_void_p), len(program.ops), C.byref(h)))
+        self._h = h
+        self.gpu_config = gpu_config or device_gpu_config(device)
+        self.profile = self._profile(profile_reps)
+        self.graph = self._profiled_dag()
+        self.plan = allocate_streams(self.graph)
+        self.schedule = make_order(self.graph, policy, self.gpu_config, seed)
+        self.seq_plan = single_stream_plan(self.graph)
+        self.seq_schedule = LaunchSchedule(tuple(self.graph.topo_sort()), "sequential")
+        self.capture(SLOT_PARALLEL, self.plan, self.schedule)
+        self.capture(SLOT_SEQUENTIAL, self.seq_plan, self.seq_schedule)
+
+    # ------------------------------------------------------------ memory
+
+    def _alloc(self, program: Program) -> None:
+        for t in program.tensors:
+            if t.alias is not None:
+                continue
+            if t.nchw_input:
+                n, h, w, c = t.shape
+                buf = torch.zeros((n, c, h, w), dtype=torch.float32, device=self.dev)
+            else:
+                buf = torch.zeros(t.shape, dtype=torch.float32, device=self.dev)
+            self._bufs[t.tid] = buf
+        root, _ = program.input.root()
+        self.input_buffer = self._bufs[root.tid]
+        oroot, ooff = program.output.root()
+        if ooff != 0 or oroot.shape != program.output.shape:
+            raise RuntimeError("graph output must be a whole buffer")
+        self.output_buffer = self._bufs[oroot.tid]
+
+    def _views(self, op):
+        x = op.inputs[0]
+        xr, xoff = x.root()
+        xb = self._bufs[xr.tid]
+        out_r, out_off = op.output.root()
+        ob = self._bufs[out_r.tid]
+        return ((xb.data_ptr(), xoff, xr.shape[-1], xr.nchw_input),
+                (ob.data_ptr(), out_off, out_r.shape[-1]))
+
+    def _weights(self, op):
+        ptrs = []
+        for arr in (op.weight, op.bias):
+            if arr is None:
+                ptrs.append(None)
+                continue
+            t = torch.from_numpy(np.ascontiguousarray(arr)).to(self.dev)
+            self._keep.append(t)
+            ptrs.append(t.data_ptr())
+        return ptrs
+
+    # ---------------------------------------------------- profile / DAG
+
+    def _profile(self, reps: int) -> list[dict]:
+        n = len(self.program.ops)
+        out = (_lib.OparaOpProfile * n)()
+        _lib.check(_lib.lib().opara_exec_profile(self._h, reps, C.cast(out, C.c_void_p)))
+        return [dict(num_blocks=p.num_blocks, threads_per_block=p.threads_per_block,
+                     shared_mem_per_block=p.shared_mem_per_block,
+                     registers_per_thread=p.registers_per_thread, isolated_us=p.isolated_us)
+                for p in out]
+
+    def _profiled_dag(self) -> ComputationGraph:
+        nodes = []
+        for k, (op, p) in enumerate(zip(self.program.ops, self.profile)):
+            d = ResourceDemand(p["threads_per_block"], p["shared_mem_per_block"],
+                               p["registers_per_thread"], p["num_blocks"])
+            nodes.append(OperatorNode(k + 1, op.name, op.op_class, d,
+                                      block_duration_us(p["isolated_us"], d, self.gpu_config)))
+        return ComputationGraph(nodes, [(u + 1, v + 1) for (u, v) in self.program.edges])
+
+    # ----------------------------------------------------------- graphs
+
+    def capture(self, slot: int, plan: StreamPlan, schedule: LaunchSchedule) -> None:
+        """Capture (plan, order) into `slot` as one multi-stream CUDA Graph."""
+        n = len(self.program.ops)
+        stream_of = np.asarray([plan.assignment[k + 1] for k in range(n)], dtype=np.int32)
+        order = np.asarray([v - 1 for v in schedule.order], dtype=np.int64)
+        sync = np.asarray([(u - 1, v - 1) for (u, v) in plan.sync_events], dtype=np.int64).reshape(-1)
+        _lib.check(_lib.lib().opara_exec_capture(self._h, slot, _lib.ptr(stream_of),
+                                                 int(plan.num_streams), _lib.ptr(order),
+                                                 _lib.ptr(sync), len(plan.sync_events)))
+
+    def replay(self, slot: int = SLOT_PARALLEL, stream: torch.cuda.Stream | None = None) -> None:
+        s = stream or torch.cuda.current_stream(self.dev)
+        _lib.check(_lib.lib().opara_exec_replay(self._h, slot, C.c_void_p(s.cuda_stream)))
+
+    def run(self, x: torch.Tensor, slot: int = SLOT_PARALLEL) -> torch.Tensor:
+        """One inference: copy `x` (NCHW) in, replay, return a copy of the output."""
+        self.input_buffer.copy_(x, non_blocking=True)
+        self.replay(slot)
+        return self.output_buffer.clone()
+
+    def run_eager(self, x: torch.Tensor, order=None) -> torch.Tensor:
+        """Launch every kernel on one stream without a graph (debugging)."""
+        self.input_buffer.copy_(x)
+        order = self.seq_schedule.order if order is None else order
+        arr = np.asarray([v - 1 for v in order], dtype=np.int64)
+        s = torch.cuda.current_stream(self.dev)
+        _lib.check(_lib.lib().opara_exec_run_eager(self._h, _lib.ptr(arr), len(arr), C.c_void_p(s.cuda_stream)))
+        return self.output_buffer.clone()
+
+    def time(self, slot: int, warmup: int = 10, iters: int = 100, flush_l2: bool = True) -> Timing:
+        """CUDA-event time of `iters` replays; L2 overwritten before each one."""
+        out = np.zeros(iters, dtype=np.float32)
+        s = torch.cuda.current_stream(self.dev)
+        flush = None
+        if flush_l2:
+            flush = torch.empty(256 << 20, dtype=torch.uint8, device=self.dev)
+        _lib.check(_lib.lib().opara_exec_time(
+            self._h, slot, warmup, iters, C.c_void_p(s.cuda_stream),
+            C.c_void_p(flush.data_ptr()) if flush is not None else None,
+            flush.numel() if flush is not None else 0, _lib.ptr(out)))
+        ms = out.tolist()
+        return Timing(float(np.median(out)), float(np.mean(out)), float(np.min(out)), ms)
+
+    def trace(self, slot: int = SLOT_PARALLEL) -> list[tuple[int, int, int]]:
+        """One replay with kernel timestamps: [(node id, start_ns, end_ns)] relative to the first start."""
+        n = len(self.program.ops)
+        st = np.zeros(n, dtype=np.int64)
+        en = np.zeros(n, dtype=np.int64)
+        s = torch.cuda.current_stream(self.dev)
+        _lib.check(_lib.lib().opara_exec_trace(self._h, slot, C.c_void_p(s.cuda_stream),
+                                               _lib.ptr(st), _lib.ptr(en)))
+        t0 = int(st.min())
+        return [(k + 1, int(st[k]) - t0, int(en[k]) - t0) for k in range(n)]
+
+    def num_launches(self, slot: int = SLOT_PARALLEL) -> int:
+        return int(_lib.lib().opara_exec_num_launches(self._h, slot))
+
+    # ------------------------------------------------------------ reports
+
+    def work(self) -> dict:
+        """Algorithmic FLOPs and bytes of one inference (DAG roofline inputs)."""
+        return {"flops": sum(op.flops for op in self.program.ops),
+                "bytes": sum(op.bytes_min for op in self.program.ops)}
+
+    def critical_path_us(self) -> float:
+        """Longest DAG path weighted by each kernel's isolated in-graph time."""
+        dist = {}
+        for v in self.graph.topo_sort():
+            base = max((dist[p] for p in self.graph.predecessors(v)), default=0.0)
+            dist[v] = base + self.profile[v - 1]["isolated_us"]
+        return max(dist.values()) if dist else 0.0
+
+    def save(self, directory) -> None:
+        """Persist the profiled DAG, plan and order (the reference's file formats)."""
+        d = Path(directory)
+        d.mkdir(parents=True, exist_ok=True)
+        (d / "graph.json").write_text(json.dumps(graph_to_dict(self.graph), indent=2, sort_keys=True) + "\n")
+        (d / "plan.json").write_text(json.dumps(plan_to_dict(self.plan, self.graph), indent=2, sort_keys=True) + "\n")
+        (d / "order.json").write_text(json.dumps({"policy": self.schedule.policy, "seed": self.schedule.seed,
+                                                  "order": list(self.schedule.order)}, indent=2, sort_keys=True) + "\n")
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.lib().opara_exec_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def compile(model: torch.nn.Module, example: torch.Tensor, *, device: int = 0, policy: str = "opara",
+            gpu_config: GpuConfig | None = None, profile_reps: int = 20,
+            seed: int | None = None) -> ScheduledGraph:
+    """Model in, scheduled graph out."""
+    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+    program = lower(model, example)
+    return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed)
+
+
+def static_dag(program: Program, gpu_config: GpuConfig | None = None) -> ComputationGraph:
+    """CPU-only DAG of a lowered program: demands from each op's launch
+    configuration (no profiling; registers 0 and a unit block time unless a GPU
+    is present).  Used by CPU tests and to produce reference fixtures."""
+    cfg = gpu_config or GPU_PRESETS["b200"]
+    nodes = []
+    dummy = []
+    for k, op in enumerate(program.ops):
+        views = ((0x1000, 0, op.inputs[0].root()[0].shape[-1], op.inputs[0].root()[0].nchw_input),
+                 (0x2000, op.output.root()[1], op.output.root()[0].shape[-1]))
+        rec = _op_record(op, views, (0x3000, 0x4000))
+        prof = _lib.OparaOpProfile()
+        _lib.check(_lib.lib().opara_op_launch_config(C.byref(rec), C.byref(prof)))
+        d = ResourceDemand(prof.threads_per_block, prof.shared_mem_per_block,
+                           prof.registers_per_thread, prof.num_blocks)
+        nodes.append(OperatorNode(k + 1, op.name, op.op_class, d, 1.0))
+    return ComputationGraph(nodes, [(u + 1, v + 1) for (u, v) in program.edges])

@@ -1,0 +1,344 @@
+"""Model -> operator DAG lowering (torch.fx).
+
+PyTorch is used here only to define the model and to trace it.  The traced
+graph is lowered to the executor's operator records:
+
+* Conv2d -> BatchNorm2d -> ReLU chains fold into one CONV2D op (BN folded in
+  float64 on the host; the kernel applies bias + ReLU in its epilogue).
+* ``torch.cat`` disappears: every concat input is produced straight into its
+  channel slice of the concatenated buffer (nested concats flatten).
+* Views (flatten, eval-mode dropout) alias their producer.
+
+The resulting DAG has one node per kernel launch, ids 1..V in trace order,
+edges from every producer of an op's input buffer region.  This is the DAG
+the scheduler (Alg. 1 / Alg. 2) sees, and the JSON the reference consumes.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.fx as fx
+import torch.nn as nn
+import torch.nn.functional as F
+
+from .dag import OpClass
+
+# opara_op_kind values (include/opara.h)
+NOP, CONV2D, MAXPOOL2D, AVGPOOL2D, GLOBAL_AVGPOOL, LINEAR = 0, 1, 2, 3, 4, 5
+
+
+@dataclass
+class Tensor:
+    """A value of the lowered program.  4-D values are NHWC channel views of a
+    root buffer; 2-D values are dense row-major [rows, features]."""
+
+    tid: int
+    shape: tuple            # (N, H, W, C) or (M, K)
+    producers: set = field(default_factory=set)   # op indices writing this region
+    alias: "Tensor | None" = None                  # concat parent
+    coff_in_alias: int = 0
+    nchw_input: bool = False                       # the graph input (dense NCHW)
+
+    def root(self) -> tuple["Tensor", int]:
+        t, off = self, 0
+        while t.alias is not None:
+            off += t.coff_in_alias
+            t = t.alias
+        return t, off
+
+
+@dataclass
+class LoweredOp:
+    kind: int
+    name: str                 # label used in the DAG (classify-table names)
+    op_class: OpClass
+    ints: dict                # named integer parameters
+    inputs: list              # [Tensor]
+    output: Tensor
+    weight: np.ndarray | None = None    # host float32, executor layout
+    bias: np.ndarray | None = None
+    flops: int = 0            # algorithmic FLOPs (2*MAC for conv/linear)
+    bytes_min: int = 0        # algorithmic bytes: inputs read once + weights + output written
+    label: str = ""           # fx node name, for reports
+
+
+class LoweringError(RuntimeError):
+    pass
+
+
+@dataclass
+class Program:
+    ops: list
+    tensors: list
+    input: Tensor
+    output: Tensor
+    edges: list               # (u, v) op indices
+
+
+def _pool_out(size, k, s, p, ceil_mode):
+    """torch's pooling output size (pooling_output_shape)."""
+    num = size + 2 * p - (k - 1) - 1 + ((s - 1) if ceil_mode else 0)
+    out = num // s + 1
+    if ceil_mode and (out - 1) * s >= size + p:
+        out -= 1
+    return out
+
+
+def _pair(v):
+    return tuple(v) if isinstance(v, (tuple, list)) else (v, v)
+
+
+def _fold_bn(conv: nn.Conv2d, bn: nn.BatchNorm2d | None):
+    w = conv.weight.detach().double().cpu()
+    b = conv.bias.detach().double().cpu() if conv.bias is not None else torch.zeros(w.shape[0], dtype=torch.float64)
+    if bn is not None:
+        scale = bn.weight.detach().double().cpu() / torch.sqrt(bn.running_var.detach().double().cpu() + bn.eps)
+        w = w * scale[:, None, None, None]
+        b = (b - bn.running_mean.detach().double().cpu()) * scale + bn.bias.detach().double().cpu()
+    # [Cout, Cin, R, S] -> [R, S, Cin, Cout] -> [K, Cout]
+    cout, cin, r, s = w.shape
+    wk = w.permute(2, 3, 1, 0).reshape(r * s * cin, cout).contiguous()
+    return wk.float().numpy(), b.float().numpy()
+
+
+class _Lowerer:
+    def __init__(self, gm: fx.GraphModule):
+        self.gm = gm
+        self.ops: list[LoweredOp] = []
+        self.tensors: list[Tensor] = []
+        self.env: dict[fx.Node, Tensor] = {}
+        self.consumed: set[fx.Node] = set()
+
+    def new_tensor(self, shape, producers=()):
+        t = Tensor(len(self.tensors), tuple(int(x) for x in shape), set(producers))
+        self.tensors.append(t)
+        return t
+
+    def emit(self, op: LoweredOp) -> None:
+        idx = len(self.ops)
+        self.ops.append(op)
+        op.output.producers = {idx}
+
+    # ----------------------------------------------------------- patterns
+
+    def _single_user(self, node, pred):
+        users = list(node.users)
+        if len(users) == 1 and pred(users[0]):
+            return users[0]
+        return None
+
+    def _is_bn(self, n):
+        return n.op == "call_module" and isinstance(self.gm.get_submodule(n.target), nn.BatchNorm2d)
+
+    def _is_relu(self, n):
+        if n.op == "call_function" and n.target in (F.relu, torch.relu):
+            return True
+        if n.op == "call_method" and n.target in ("relu", "relu_"):
+            return True
+        return n.op == "call_module" and isinstance(self.gm.get_submodule(n.target), nn.ReLU)
+
+    def lower_conv(self, node, conv: nn.Conv2d):
+        if conv.groups != 1 or _pair(conv.dilation) != (1, 1):
+            raise LoweringError(f"{node.name}: grouped/dilated conv not supported by CONV2D")
+        if conv.padding_mode != "zeros" or isinstance(conv.padding, str):
+            raise LoweringError(f"{node.name}: only explicit zero padding is supported")
+        x = self.env[node.args[0]]
+        bn_node = self._single_user(node, self._is_bn)
+        tail = node
+        bn = None
+        if bn_node is not None:
+            bn = self.gm.get_submodule(bn_node.target)
+            self.consumed.add(bn_node)
+            tail = bn_node
+        relu_node = self._single_user(tail, self._is_relu)
+        if relu_node is not None:
+            self.consumed.add(relu_node)
+            tail = relu_node
+        n, h, w, cin = x.shape
+        r, s = conv.kernel_size
+        sh, sw = _pair(conv.stride)
+        ph, pw = _pair(conv.padding)
+        oh = (h + 2 * ph - r) // sh + 1
+        ow = (w + 2 * pw - s) // sw + 1
+        cout = conv.out_channels
+        out = self.new_tensor((n, oh, ow, cout))
+        wk, b = _fold_bn(conv, bn)
+        macs = n * oh * ow * cout * r * s * cin
+        op = LoweredOp(CONV2D, "conv", OpClass.COMPUTE,
+                       dict(N=n, H=h, W=w, Cin=cin, OH=oh, OW=ow, Cout=cout, R=r, S=s, sh=sh,
+                            sw=sw, ph=ph, pw=pw, relu=int(relu_node is not None)),
+                       [x], out, wk, b, flops=2 * macs,
+                       bytes_min=4 * (n * h * w * cin + wk.size + b.size + n * oh * ow * cout),
+                       label=node.name)
+        self.emit(op)
+        self.env[tail] = out
+
+    def lower_pool(self, node, is_max, k, s, p, ceil_mode, include_pad=True, dilation=1):
+        if _pair(dilation) != (1, 1):
+            raise LoweringError(f"{node.name}: dilated pooling not supported")
+        x = self.env[node.args[0]]
+        kh, kw = _pair(k)
+        sh, sw = _pair(s if s not in (None, ()) else k)
+        ph, pw = _pair(p)
+        n, h, w, c = x.shape
+        oh = _pool_out(h, kh, sh, ph, ceil_mode)
+        ow = _pool_out(w, kw, sw, pw, ceil_mode)
+        out = self.new_tensor((n, oh, ow, c))
+        op = LoweredOp(MAXPOOL2D if is_max else AVGPOOL2D, "pool", OpClass.MEMORY,
+                       dict(N=n, H=h, W=w, C=c, OH=oh, OW=ow, kh=kh, kw=kw, sh=sh, sw=sw, ph=ph,
+                            pw=pw, include_pad=int(include_pad)),
+                       [x], out, flops=n * oh * ow * c * kh * kw,
+                       bytes_min=4 * (n * h * w * c + n * oh * ow * c), label=node.name)
+        self.emit(op)
+        self.env[node] = out
+
+    def lower_gap(self, node):
+        x = self.env[node.args[0]]
+        n, h, w, c = x.shape
+        out = self.new_tensor((n, c))
+        op = LoweredOp(GLOBAL_AVGPOOL, "pool", OpClass.MEMORY, dict(N=n, H=h, W=w, C=c), [x], out,
+                       flops=n * h * w * c, bytes_min=4 * (n * h * w * c + n * c), label=node.name)
+        self.emit(op)
+        self.env[node] = out
+
+    def lower_linear(self, node, lin: nn.Linear):
+        x = self.env[node.args[0]]
+        if len(x.shape) != 2:
+            raise LoweringError(f"{node.name}: linear expects a [rows, features] input")
+        m, k = x.shape
+        nout = lin.out_features
+        act = 0
+        tail = node
+        relu_node = self._single_user(node, self._is_relu)
+        if relu_node is not None:
+            act = 1
+            self.consumed.add(relu_node)
+            tail = relu_node
+        out = self.new_tensor((m, nout))
+        wt = lin.weight.detach().float().cpu().contiguous().numpy()
+        b = lin.bias.detach().float().cpu().numpy() if lin.bias is not None else None
+        op = LoweredOp(LINEAR, "gemm", OpClass.COMPUTE, dict(M=m, K=k, N=nout, act=act), [x], out,
+                       wt, b, flops=2 * m * k * nout,
+                       bytes_min=4 * (m * k + wt.size + (0 if b is None else b.size) + m * nout),
+                       label=node.name)
+        self.emit(op)
+        self.env[tail] = out
+
+    def lower_cat(self, node):
+        parts = node.args[0]
+        dim = node.args[1] if len(node.args) > 1 else node.kwargs.get("dim", 0)
+        ins = [self.env[p] for p in parts]
+        if any(len(t.shape) != 4 for t in ins) or dim not in (1, -3):
+            raise LoweringError(f"{node.name}: only channel concat of NCHW tensors is supported")
+        n, h, w = ins[0].shape[:3]
+        ctot = sum(t.shape[3] for t in ins)
+        out = self.new_tensor((n, h, w, ctot))
+        off = 0
+        for t in ins:
+            if t.alias is not None or t.nchw_input:
+                raise LoweringError(f"{node.name}: concat input already aliased (needs a copy op)")
+            t.alias = out
+            t.coff_in_alias = off
+            off += t.shape[3]
+        # The concat stays a DAG node (the paper's operator graph has it) but
+        # launches nothing: its producers already wrote their slices, so it is
+        # a pure join — capture applies its waits and records only.
+        self.emit(LoweredOp(NOP, "concat", OpClass.MEMORY, {}, ins, out, label=node.name))
+        self.env[node] = out
+
+    # ------------------------------------------------------------- driver
+
+    def run(self, example: torch.Tensor) -> Program:
+        if example.dim() != 4:
+            raise LoweringError("example input must be a 4-D NCHW tensor")
+        inp = None
+        for node in self.gm.graph.nodes:
+            if node in self.consumed:
+                continue
+            if node.op == "placeholder":
+                if inp is not None:
+                    raise LoweringError("single-input models only")
+                n, c, h, w = example.shape
+                inp = self.new_tensor((n, h, w, c))
+                inp.nchw_input = True
+                self.env[node] = inp
+            elif node.op == "output":
+                res = node.args[0]
+                if isinstance(res, (tuple, list)):
+                    res = res[0]
+                self.env["__out__"] = self.env[res]
+            elif node.op == "call_module":
+                mod = self.gm.get_submodule(node.target)
+                if isinstance(mod, nn.Conv2d):
+                    self.lower_conv(node, mod)
+                elif isinstance(mod, nn.MaxPool2d):
+                    self.lower_pool(node, True, mod.kernel_size, mod.stride, mod.padding,
+                                    mod.ceil_mode, dilation=mod.dilation)
+                elif isinstance(mod, nn.AvgPool2d):
+                    if mod.divisor_override is not None:
+                        raise LoweringError(f"{node.name}: divisor_override unsupported")
+                    self.lower_pool(node, False, mod.kernel_size, mod.stride, mod.padding,
+                                    mod.ceil_mode, mod.count_include_pad)
+                elif isinstance(mod, nn.AdaptiveAvgPool2d):
+                    if _pair(mod.output_size) != (1, 1):
+                        raise LoweringError(f"{node.name}: only global adaptive pooling")
+                    self.lower_gap(node)
+                elif isinstance(mod, (nn.Dropout, nn.Identity)):
+                    self.env[node] = self.env[node.args[0]]
+                elif isinstance(mod, nn.Linear):
+                    self.lower_linear(node, mod)
+                else:
+                    raise LoweringError(f"{node.name}: unsupported module {type(mod).__name__}")
+            elif node.op == "call_function":
+                tgt = node.target
+                if tgt is torch.cat:
+                    self.lower_cat(node)
+                elif tgt is torch.flatten:
+                    x = self.env[node.args[0]]
+                    if len(x.shape) == 2:
+                        self.env[node] = x
+                    elif len(x.shape) == 4 and x.shape[1] == 1 and x.shape[2] == 1:
+                        raise LoweringError(f"{node.name}: flatten of an unpooled 1x1 map")
+                    else:
+                        raise LoweringError(f"{node.name}: flatten of a spatial map unsupported")
+                elif tgt is F.avg_pool2d:
+                    a = node.args
+                    kw = node.kwargs
+                    k = a[1] if len(a) > 1 else kw["kernel_size"]
+                    s = a[2] if len(a) > 2 else kw.get("stride", None)
+                    p = a[3] if len(a) > 3 else kw.get("padding", 0)
+                    cm = a[4] if len(a) > 4 else kw.get("ceil_mode", False)
+                    cip = a[5] if len(a) > 5 else kw.get("count_include_pad", True)
+                    self.lower_pool(node, False, k, s, p, cm, cip)
+                elif tgt is F.max_pool2d:
+                    a = node.args
+                    kw = node.kwargs
+                    k = a[1] if len(a) > 1 else kw["kernel_size"]
+                    s = a[2] if len(a) > 2 else kw.get("stride", None)
+                    p = a[3] if len(a) > 3 else kw.get("padding", 0)
+                    d = a[4] if len(a) > 4 else kw.get("dilation", 1)
+                    cm = a[5] if len(a) > 5 else kw.get("ceil_mode", False)
+                    self.lower_pool(node, True, k, s, p, cm, dilation=d)
+                elif tgt in (F.dropout,):
+                    self.env[node] = self.env[node.args[0]]
+                else:
+                    raise LoweringError(f"{node.name}: unsupported function {tgt}")
+            else:
+                raise LoweringError(f"{node.name}: unsupported fx op {node.op}")
+        out = self.env["__out__"]
+        edges = set()
+        for v, op in enumerate(self.ops):
+            for t in op.inputs:
+                for u in t.producers:
+                    edges.add((u, v))
+        return Program(self.ops, self.tensors, inp, out, sorted(edges))
+
+
+def lower(model: nn.Module, example: torch.Tensor) -> Program:
+    """Trace `model` with torch.fx and lower it to executor operators."""
+    model = model.eval()
+    gm = fx.symbolic_trace(model)
+    return _Lowerer(gm).run(example)
