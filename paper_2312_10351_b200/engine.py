@@ -208,6 +208,34 @@ class ScheduledGraph:
         self.replay(slot)
         return self.output_buffer.clone()
 
+    def run_host(self, x_host: torch.Tensor, out_host: torch.Tensor, slot: int = SLOT_PARALLEL) -> None:
+        """Host-buffer inference (asynchronous): H2D copy of `x_host` (pinned
+        NCHW), replay, D2H copy of the output into `out_host` (pinned)."""
+        self.input_buffer.copy_(x_host, non_blocking=True)
+        self.replay(slot)
+        out_host.copy_(self.output_buffer, non_blocking=True)
+
+    def time_host_roundtrip(self, x: torch.Tensor, warmup: int = 10, iters: int = 100,
+                            slot: int = SLOT_PARALLEL) -> dict:
+        """Time run_host end to end (CUDA events bracketing H2D + replay + D2H)."""
+        x_host = x.detach().to(torch.float32).contiguous().pin_memory()
+        out_host = torch.empty(self.output_buffer.shape, dtype=self.output_buffer.dtype).pin_memory()
+        s = torch.cuda.current_stream(self.dev)
+        for _ in range(warmup):
+            self.run_host(x_host, out_host, slot)
+        s.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(iters)]
+        for a, b in evs:
+            a.record(s)
+            self.run_host(x_host, out_host, slot)
+            b.record(s)
+        s.synchronize()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        return {"seconds": sum(ms) / 1e3, "median_ms": float(np.median(ms)),
+                "h2d_bytes": x_host.numel() * x_host.element_size(),
+                "d2h_bytes": out_host.numel() * out_host.element_size()}
+
     def run_eager(self, x: torch.Tensor, order=None) -> torch.Tensor:
         """Launch every kernel on one stream without a graph (debugging)."""
         self.input_buffer.copy_(x)
