@@ -5,9 +5,11 @@
 //   B = folded weights [K][Cout].  Epilogue: + folded-BN bias, ReLU, store into
 //   the output channel view (concat slice).
 //
-// This is the exact-fp32 engine used for the fp32 parity configs; the tensor-
-// core (tcgen05) engines live in conv_tc.cu.  Grids are bounded by the tile
-// choice so independent branches can co-reside.
+// Batch-1 layers are small in M (49..12544 pixels), so the launcher spreads
+// one conv over a bounded number of CTAs with split-K: every split writes its
+// partial tile to a private workspace, and the last split to arrive (per-tile
+// arrival counter) reduces the partials in split order — deterministic — and
+// runs the epilogue.  The tensor-core engines live in conv_tc.cu.
 
 #include "device_common.cuh"
 #include "ops.h"
@@ -21,25 +23,31 @@ struct ConvArgs {
   const float* __restrict__ w;
   const float* __restrict__ bias;
   float* __restrict__ out;
+  float* __restrict__ ws;       // [splits][M][Cout] partials (split-K only)
+  unsigned* __restrict__ cnt;   // per output tile arrival counters (split-K only)
   int N, H, W, Cin, in_cs, in_coff;
   int OH, OW, Cout, out_cs, out_coff;
   int R, S, sh, sw, ph, pw;
   int relu;
   int M, K;
+  int splits, kt_per_split;
   // input element (b, ih, iw, c) lives at in[b*sN + ih*sH + iw*sW + c*sC + in_coff]
   int64_t sN, sH, sW, sC;
 };
 
 constexpr int BK = 16;
 
-template <int BM, int BN, int TM, int TN>
+template <int BM, int BN, int TM, int TN, bool kVec>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     conv2d_f32_simt(ConvArgs a, unsigned long long* trace) {
   constexpr int T = (BM / TM) * (BN / TN);
   static_assert(T % BK == 0, "thread count must be a multiple of BK");
-  constexpr int A_PER = BM * BK / T;
+  // scalar gather: one k lane per thread; vector gather: one 4-channel chunk
+  constexpr int A_LANES = kVec ? BK / 4 : BK;
+  constexpr int A_ROWS = T / A_LANES;
+  constexpr int A_PER = (BM + A_ROWS - 1) / A_ROWS;  // rows past BM idle (small tiles)
+  static_assert(BM % A_ROWS == 0 || A_ROWS % BM == 0, "bad A split");
   constexpr int B_PER = BK * BN / T;
-  constexpr int A_ROWS = T / BK;  // m rows covered per pass
   __shared__ __align__(16) float As[2][BK][BM + 4];
   __shared__ __align__(16) float Bs[2][BK][BN + 4];
   trace_begin(trace);
@@ -48,14 +56,14 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int tx = tid % (BN / TN), ty = tid / (BN / TN);
 
-  // Per-thread A gather coordinates: fixed k lane, A_PER output pixels.
-  const int a_k = tid % BK;
+  const int a_lane = tid % A_LANES;
+  const int a_row = tid / A_LANES;
   int a_base[A_PER], a_ih0[A_PER], a_iw0[A_PER];
   const int ohw = a.OH * a.OW;
 #pragma unroll
   for (int j = 0; j < A_PER; ++j) {
-    const int m = m0 + tid / BK + j * A_ROWS;
-    if (m < a.M) {
+    const int m = m0 + a_row + j * A_ROWS;
+    if (m < a.M && a_row + j * A_ROWS < BM) {
       const int b = m / ohw, rem = m - b * ohw;
       const int oh = rem / a.OW, ow = rem - oh * a.OW;
       a_base[j] = b;
@@ -71,9 +79,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   const int b_k0 = tid / BN;
   constexpr int B_KSTEP = T / BN;
 
-  float ra[A_PER], rb[B_PER];
+  constexpr int AV = kVec ? 4 : 1;
+  float ra[A_PER][AV], rb[B_PER];
   auto load_tile = [&](int k0) {
-    const int k = k0 + a_k;
+    const int k = k0 + a_lane * AV;
     int c = 0, r = 0, s = 0;
     const bool kin = k < a.K;
     if (kin) {
@@ -85,10 +94,14 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 #pragma unroll
     for (int j = 0; j < A_PER; ++j) {
       const int ih = a_ih0[j] + r, iw = a_iw0[j] + s;
-      float v = 0.f;
-      if (kin && a_base[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W)
-        v = __ldg(a.in + a_base[j] * a.sN + ih * a.sH + iw * a.sW + c * a.sC + a.in_coff);
-      ra[j] = v;
+      const bool ok = kin && a_base[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+      const float* src = a.in + a_base[j] * a.sN + ih * a.sH + iw * a.sW + c * a.sC + a.in_coff;
+      if constexpr (kVec) {
+        float4 v = ok ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ra[j][0] = v.x; ra[j][1] = v.y; ra[j][2] = v.z; ra[j][3] = v.w;
+      } else {
+        ra[j][0] = ok ? __ldg(src) : 0.f;
+      }
     }
 #pragma unroll
     for (int j = 0; j < B_PER; ++j) {
@@ -99,7 +112,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   };
   auto store_tile = [&](int buf) {
 #pragma unroll
-    for (int j = 0; j < A_PER; ++j) As[buf][a_k][tid / BK + j * A_ROWS] = ra[j];
+    for (int j = 0; j < A_PER; ++j)
+      if (a_row + j * A_ROWS < BM)
+#pragma unroll
+        for (int e = 0; e < AV; ++e) As[buf][a_lane * AV + e][a_row + j * A_ROWS] = ra[j][e];
 #pragma unroll
     for (int j = 0; j < B_PER; ++j) Bs[buf][b_k0 + j * B_KSTEP][b_n] = rb[j];
   };
@@ -111,26 +127,62 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
   const int ktiles = (a.K + BK - 1) / BK;
-  load_tile(0);
-  store_tile(0);
-  __syncthreads();
-  for (int kt = 0; kt < ktiles; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float av[TM], bv[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) av[i] = As[buf][kk][ty * TM + i];
-#pragma unroll
-      for (int j = 0; j < TN; ++j) bv[j] = Bs[buf][kk][tx * TN + j];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-    }
-    if (kt + 1 < ktiles) store_tile(buf ^ 1);
+  const int kt_begin = blockIdx.z * a.kt_per_split;
+  const int kt_end = min(ktiles, kt_begin + a.kt_per_split);
+  if (kt_begin < kt_end) {
+    load_tile(kt_begin * BK);
+    store_tile(0);
     __syncthreads();
+    for (int kt = kt_begin; kt < kt_end; ++kt) {
+      const int buf = (kt - kt_begin) & 1;
+      if (kt + 1 < kt_end) load_tile((kt + 1) * BK);
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        float av[TM], bv[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) av[i] = As[buf][kk][ty * TM + i];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) bv[j] = Bs[buf][kk][tx * TN + j];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      }
+      if (kt + 1 < kt_end) store_tile(buf ^ 1);
+      __syncthreads();
+    }
+  }
+
+  if (a.splits > 1) {
+    // publish this split's partial tile, then let the last arrival reduce
+    const int64_t plane = static_cast<int64_t>(a.M) * a.Cout;
+    float* mine = a.ws + blockIdx.z * plane;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int m = m0 + ty * TM + i;
+      if (m >= a.M) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int n = n0 + tx * TN + j;
+        if (n < a.Cout) __stcg(mine + static_cast<int64_t>(m) * a.Cout + n, acc[i][j]);
+      }
+    }
+    if (!splitk_arrive_last(a.cnt + blockIdx.x + blockIdx.y * gridDim.x, a.splits)) {
+      trace_end(trace);
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int m = m0 + ty * TM + i;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int n = n0 + tx * TN + j;
+        float s = 0.f;
+        if (m < a.M && n < a.Cout)
+          for (int z = 0; z < a.splits; ++z) s += __ldcg(a.ws + z * plane + static_cast<int64_t>(m) * a.Cout + n);
+        acc[i][j] = s;
+      }
+    }
   }
 
 #pragma unroll
@@ -153,40 +205,64 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 
 struct Variant {
   int bm, bn;
-  const void* func;
+  const void* func[2];  // [scalar gather, 4-channel vector gather]
   int threads;
 };
 
 template <int BM, int BN, int TM, int TN>
 Variant make_variant() {
-  return {BM, BN, reinterpret_cast<const void*>(&conv2d_f32_simt<BM, BN, TM, TN>),
+  return {BM, BN,
+          {reinterpret_cast<const void*>(&conv2d_f32_simt<BM, BN, TM, TN, false>),
+           reinterpret_cast<const void*>(&conv2d_f32_simt<BM, BN, TM, TN, true>)},
           (BM / TM) * (BN / TN)};
 }
 
 const Variant* variants(int* count) {
   static const Variant v[] = {
-      make_variant<64, 64, 4, 4>(),  // 0
-      make_variant<32, 64, 2, 4>(),  // 1
-      make_variant<64, 32, 4, 2>(),  // 2
-      make_variant<32, 32, 2, 2>(),  // 3  (256 threads, 2x2 micro tiles)
-      make_variant<128, 64, 8, 4>(), // 4
-      make_variant<16, 64, 1, 4>(),  // 5
+      make_variant<64, 64, 4, 4>(),   // 0
+      make_variant<32, 64, 2, 4>(),   // 1
+      make_variant<64, 32, 4, 2>(),   // 2
+      make_variant<32, 32, 2, 2>(),   // 3
+      make_variant<128, 64, 8, 4>(),  // 4
+      make_variant<16, 64, 1, 4>(),   // 5
   };
   *count = static_cast<int>(sizeof(v) / sizeof(v[0]));
   return v;
 }
 
-// Pick the largest tile that still yields enough CTAs to spread one branch
-// over a bounded share of the 148 SMs.
-int auto_variant(int64_t M, int64_t N) {
+struct Choice {
+  int id, splits, kt_per_split;
+};
+
+// Latency-first tiling for one branch: largest tile whose grid, after
+// split-K, reaches `target` CTAs while every split keeps >= 4 k-tiles.
+Choice auto_choice(int64_t M, int64_t N, int64_t K, int64_t target) {
   int count = 0;
   const Variant* v = variants(&count);
+  const int64_t ktiles = (K + BK - 1) / BK;
   const int prefs[] = {4, 0, 1, 2, 3, 5};
+  Choice best{3, 1, static_cast<int>(ktiles)};
+  double best_cost = 1e30;
   for (int id : prefs) {
-    const int64_t ctas = ((M + v[id].bm - 1) / v[id].bm) * ((N + v[id].bn - 1) / v[id].bn);
-    if (ctas >= 96) return id;
+    const int64_t base = ((M + v[id].bm - 1) / v[id].bm) * ((N + v[id].bn - 1) / v[id].bn);
+    int64_t splits = std::max<int64_t>(1, (target + base - 1) / base);
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, ktiles / 4));
+    splits = std::min<int64_t>(splits, 32);
+    const int64_t kps = (ktiles + splits - 1) / splits;
+    splits = (ktiles + kps - 1) / kps;
+    const int64_t ctas = base * splits;
+    // cost model: waves of one CTA's k-loop over a 148-SM, 2-CTA/SM machine,
+    // plus a reduction term when split
+    const double waves = std::ceil(static_cast<double>(ctas) / (148.0 * 2.0));
+    const double per_cta = static_cast<double>(kps) * v[id].bm * v[id].bn;
+    const double cost = waves * per_cta * 1.0 + (splits > 1 ? 0.15 * splits * v[id].bm * v[id].bn : 0.0) +
+                        2000.0 * splits;  // fixed overhead per split pass
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = {id, static_cast<int>(splits), static_cast<int>(kps)};
+    }
   }
-  return M <= 16 ? 5 : 3;
+  return best;
 }
 
 }  // namespace
@@ -207,7 +283,8 @@ opara_status launch_conv2d(const opara_op& op, cudaStream_t s, unsigned long lon
   if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "conv2d simt engine: fp32 only");
   a.M = a.N * a.OH * a.OW;
   a.K = a.R * a.S * a.Cin;
-  if (op.i[20]) {  // dense NCHW input
+  const bool nchw = op.i[20] != 0;
+  if (nchw) {  // dense NCHW input
     a.sC = static_cast<int64_t>(a.H) * a.W;
     a.sW = 1;
     a.sH = a.W;
@@ -222,15 +299,36 @@ opara_status launch_conv2d(const opara_op& op, cudaStream_t s, unsigned long lon
   if (a.M <= 0 || a.Cout <= 0 || a.K <= 0) return fail(OPARA_ERR_VALUE, "conv2d: empty shape");
   int count = 0;
   const Variant* v = variants(&count);
-  int id = op.variant;
-  if (id < 0 || id >= count) id = auto_variant(a.M, a.Cout);
+  const int64_t target = op.i[21] > 0 ? op.i[21] : 296;
+  Choice ch = auto_choice(a.M, a.Cout, a.K, target);
+  if (op.variant >= 0 && op.variant < count) {
+    ch.id = op.variant;
+    ch.splits = op.i[19] > 1 ? static_cast<int>(op.i[19]) : 1;
+    const int ktiles = (a.K + BK - 1) / BK;
+    ch.kt_per_split = (ktiles + ch.splits - 1) / ch.splits;
+    ch.splits = (ktiles + ch.kt_per_split - 1) / ch.kt_per_split;
+  }
+  a.splits = ch.splits;
+  a.kt_per_split = ch.kt_per_split;
+  const bool vec = !nchw && a.Cin % 4 == 0 && a.in_cs % 4 == 0 && a.in_coff % 4 == 0 &&
+                   reinterpret_cast<uintptr_t>(a.in) % 16 == 0;
   LaunchCfg c;
-  c.func = v[id].func;
-  c.grid = dim3(ceil_div(a.M, v[id].bm), ceil_div(a.Cout, v[id].bn), 1);
-  c.block = dim3(v[id].threads, 1, 1);
+  c.func = v[ch.id].func[vec ? 1 : 0];
+  c.grid = dim3(ceil_div(a.M, v[ch.id].bm), ceil_div(a.Cout, v[ch.id].bn), ch.splits);
+  c.block = dim3(v[ch.id].threads, 1, 1);
   c.smem = 0;
+  const int64_t tiles = static_cast<int64_t>(c.grid.x) * c.grid.y;
+  c.workspace = ch.splits > 1 ? splitk_workspace_bytes(static_cast<int64_t>(a.M) * a.Cout * ch.splits, tiles) : 0;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
+  if (ch.splits > 1) {
+    if (!op.p[7]) return fail(OPARA_ERR_INTERNAL, "conv2d: split-K workspace missing");
+    a.ws = static_cast<float*>(op.p[7]);
+    a.cnt = splitk_counters(op.p[7], static_cast<int64_t>(a.M) * a.Cout * ch.splits);
+  } else {
+    a.ws = nullptr;
+    a.cnt = nullptr;
+  }
   void* args[] = {&a, &trace};
   return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, c.smem, s), "conv2d launch");
 }

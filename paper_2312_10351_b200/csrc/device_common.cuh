@@ -22,6 +22,26 @@ __device__ __forceinline__ void trace_end(unsigned long long* t) {
   if (t && (threadIdx.x & 31) == 0) atomicMax(t + 1, global_ns());
 }
 
+// Split-K arrival: every thread has stored its partials (st.global.cg); the
+// CTA fences, one thread bumps the tile's arrival counter, and the CTA that
+// arrives last (returns true) owns the reduction.  The last arrival resets the
+// counter so the next graph replay starts from zero.  Reductions then read the
+// partials with ld.global.cg in split order, so results are deterministic.
+__device__ __forceinline__ bool splitk_arrive_last(unsigned* cnt, int splits) {
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const unsigned prev = atomicAdd(cnt, 1u);
+    s_last = prev == static_cast<unsigned>(splits - 1);
+    if (s_last) atomicExch(cnt, 0u);
+  }
+  __syncthreads();
+  const bool last = s_last != 0;
+  if (last) __threadfence();
+  return last;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

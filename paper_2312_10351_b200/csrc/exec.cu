@@ -34,7 +34,8 @@ opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* t
     case OPARA_OP_NOP:
       if (cfg) *cfg = LaunchCfg{};
       return OPARA_OK;
-    case OPARA_OP_CONV2D: return launch_conv2d(op, s, trace, cfg, dry);
+    case OPARA_OP_CONV2D:
+      return op.i[22] == 1 ? launch_conv2d_tc(op, s, trace, cfg, dry) : launch_conv2d(op, s, trace, cfg, dry);
     case OPARA_OP_MAXPOOL2D:
     case OPARA_OP_AVGPOOL2D: return launch_pool2d(op, s, trace, cfg, dry);
     case OPARA_OP_GLOBAL_AVGPOOL: return launch_global_avgpool(op, s, trace, cfg, dry);
@@ -71,9 +72,11 @@ struct opara_exec {
   std::map<int32_t, Graph> graphs;         // plain replay graphs
   std::map<int32_t, Graph> traced_graphs;  // same plan, kernels write timestamps
   unsigned long long* trace_buf = nullptr;  // 2 * ops.size()
+  std::vector<void*> workspaces;
 
   ~opara_exec() {
     cudaSetDevice(device);
+    for (void* w : workspaces) cudaFree(w);
     for (auto* m : {&graphs, &traced_graphs})
       for (auto& kv : *m) {
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -234,6 +237,17 @@ opara_status opara_exec_create(int32_t device, const opara_op* ops, int64_t n, o
     if (st != OPARA_OK) {
       delete ex;
       return fail(st, "op " + std::to_string(i) + ": " + opara::g_last_error);
+    }
+    if (c.workspace > 0) {  // private per-op scratch: concurrent branches never share it
+      void* ws = nullptr;
+      cudaError_t e = cudaMalloc(&ws, c.workspace);
+      if (e == cudaSuccess) e = cudaMemset(ws, 0, c.workspace);
+      if (e != cudaSuccess) {
+        delete ex;
+        return cuda_fail(e, "workspace allocation");
+      }
+      ex->workspaces.push_back(ws);
+      ex->ops[i].p[7] = ws;
     }
   }
   *out = ex;

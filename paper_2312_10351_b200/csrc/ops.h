@@ -9,9 +9,13 @@
 //                 6 OH, 7 OW, 8 Cout, 9 out_cstride, 10 out_coff,
 //                 11 R, 12 S, 13 stride_h, 14 stride_w, 15 pad_h, 16 pad_w,
 //                 17 relu, 18 dtype (0 f32), 19 split_k (1),
-//                 20 in_nchw (1: input is a dense NCHW tensor, e.g. the graph input)
-//              p: 0 in, 1 weight [R*S*Cin][Cout] (k = (r*S + s)*Cin + c), 2 bias [Cout], 3 out
-//              variant: tile id (conv_simt.cu), -1 = auto
+//                 20 in_nchw (1: input is a dense NCHW tensor, e.g. the graph input),
+//                 21 target CTAs for split-K (0 = default), 22 engine (0 SIMT fp32,
+//                 1 tcgen05 3xTF32)
+//              p: 0 in, 1 weight: engine 0 [R*S*Cin][Cout] (k = (r*S + s)*Cin + c);
+//                 engine 1 packed tf32 hi/lo UMMA images (conv_tc.cu), 2 bias [Cout], 3 out,
+//                 7 split-K workspace (executor-owned)
+//              variant: tile id, -1 = auto
 // MAXPOOL2D /  i: 0 N, 1 H, 2 W, 3 C, 4 in_cstride, 5 in_coff, 6 OH, 7 OW, 8 out_cstride,
 // AVGPOOL2D       9 out_coff, 10 kh, 11 kw, 12 sh, 13 sw, 14 ph, 15 pw,
 //                 16 count_include_pad (avg), 18 dtype
@@ -35,7 +39,17 @@ struct LaunchCfg {
   dim3 grid{1, 1, 1};
   dim3 block{1, 1, 1};
   size_t smem = 0;
+  size_t workspace = 0;  // private device scratch the executor allocates into op.p[7]
 };
+
+// Split-K workspace: `floats` partial values, then one u32 arrival counter per
+// output tile (zeroed once at allocation; the last arrival re-zeroes it).
+inline size_t splitk_workspace_bytes(int64_t floats, int64_t tiles) {
+  return static_cast<size_t>(((floats * 4 + 255) / 256) * 256 + tiles * 4);
+}
+inline unsigned* splitk_counters(void* ws, int64_t floats) {
+  return reinterpret_cast<unsigned*>(static_cast<char*>(ws) + ((floats * 4 + 255) / 256) * 256);
+}
 
 // trace: nullable device pointer to two u64 slots (min start, max end ns).
 // dry: only fill `cfg` (no device access), used for profiles on CPU hosts.
@@ -43,6 +57,7 @@ using Launcher = opara_status (*)(const opara_op& op, cudaStream_t s, unsigned l
                                   LaunchCfg* cfg, bool dry);
 
 opara_status launch_conv2d(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+opara_status launch_conv2d_tc(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
 opara_status launch_pool2d(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
 opara_status launch_global_avgpool(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*,
                                    bool);

@@ -57,7 +57,39 @@ def block_duration_us(isolated_us: float, d: ResourceDemand, cfg: GpuConfig) -> 
     return max(isolated_us / waves, 0.001)
 
 
-def _op_record(op, views, weights) -> _lib.OparaOp:
+CONV_ENGINES = {"simt": 0, "tc": 1}
+
+
+def tf32_rna(x: np.ndarray) -> np.ndarray:
+    """fp32 -> tf32 round-to-nearest, ties away (cvt.rna.tf32.f32), as fp32."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    b = (b + np.uint32(0x1000)) & np.uint32(0xFFFFE000)
+    return b.view(np.float32)
+
+
+def pack_conv_weights_tf32x3(wk: np.ndarray) -> np.ndarray:
+    """[K][Cout] fp32 conv weights -> the tcgen05 engine's W operand images.
+
+    Rows = output channels (UMMA M, padded to 128-row tiles), columns = k
+    (padded to 16-element blocks).  Every (m-tile, k-block) becomes one
+    contiguous 16 KiB record: the tf32 hi plane then the tf32 lo plane, each in
+    the no-swizzle K-major core-matrix order [chunk(4)][row group(16)][row(8)]
+    [4 fp32] that conv_tc.cu's smem descriptors (LBO 2048 B, SBO 128 B) expect.
+    """
+    k, cout = wk.shape
+    mt, kb = -(-cout // 128), -(-k // 16)
+    w = np.zeros((mt * 128, kb * 16), dtype=np.float32)
+    w[:cout, :k] = wk.T
+    hi = tf32_rna(w)
+    lo = tf32_rna(w - hi)
+
+    def image(x):
+        return x.reshape(mt, 16, 8, kb, 4, 4).transpose(0, 3, 4, 1, 2, 5)
+
+    return np.ascontiguousarray(np.stack([image(hi), image(lo)], axis=2)).reshape(-1)
+
+
+def _op_record(op, views, weights, conv_engine: int = 1) -> _lib.OparaOp:
     """Fill the POD launch record of one lowered op (layouts: csrc/ops.h)."""
     rec = _lib.OparaOp()
     rec.kind = op.kind
@@ -69,7 +101,8 @@ def _op_record(op, views, weights) -> _lib.OparaOp:
     i = rec.i
     if op.kind == CONV2D:
         vals = [q["N"], q["H"], q["W"], q["Cin"], ics, icoff, q["OH"], q["OW"], q["Cout"], ocs, ocoff,
-                q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], 0, 1, int(inchw)]
+                q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], 0, 1, int(inchw), 0,
+                conv_engine]
         rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
     elif op.kind in (MAXPOOL2D, AVGPOOL2D):
         vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff, q["OH"], q["OW"], ocs, ocoff, q["kh"],
@@ -100,18 +133,20 @@ class ScheduledGraph:
     """A compiled model: profiled DAG, Opara plan + order, captured graphs."""
 
     def __init__(self, program: Program, device: int, policy: str = "opara",
-                 gpu_config: GpuConfig | None = None, profile_reps: int = 20, seed: int | None = None):
+                 gpu_config: GpuConfig | None = None, profile_reps: int = 20, seed: int | None = None,
+                 conv_engine: str = "tc"):
         if not torch.cuda.is_available():
             raise RuntimeError("ScheduledGraph needs a CUDA device (there is no CPU fallback)")
         self.program = program
         self.device = device
+        self.conv_engine = CONV_ENGINES[conv_engine]
         self.dev = torch.device("cuda", device)
         self._bufs: dict[int, torch.Tensor] = {}
         self._keep: list[torch.Tensor] = []
         self._alloc(program)
         recs = (_lib.OparaOp * len(program.ops))()
         for k, op in enumerate(program.ops):
-            recs[k] = _op_record(op, self._views(op), self._weights(op))
+            recs[k] = _op_record(op, self._views(op), self._weights(op), self.conv_engine)
         self._recs = recs
         L = _lib.lib()
         h = C.c_void_p()
@@ -157,7 +192,10 @@ class ScheduledGraph:
 
     def _weights(self, op):
         ptrs = []
-        for arr in (op.weight, op.bias):
+        weight = op.weight
+        if op.kind == CONV2D and self.conv_engine == 1:
+            weight = pack_conv_weights_tf32x3(op.weight)
+        for arr in (weight, op.bias):
             if arr is None:
                 ptrs.append(None)
                 continue
@@ -312,14 +350,15 @@ class ScheduledGraph:
 
 def compile(model: torch.nn.Module, example: torch.Tensor, *, device: int = 0, policy: str = "opara",
             gpu_config: GpuConfig | None = None, profile_reps: int = 20,
-            seed: int | None = None) -> ScheduledGraph:
+            seed: int | None = None, conv_engine: str = "tc") -> ScheduledGraph:
     """Model in, scheduled graph out."""
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     program = lower(model, example)
-    return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed)
+    return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine)
 
 
-def static_dag(program: Program, gpu_config: GpuConfig | None = None) -> ComputationGraph:
+def static_dag(program: Program, gpu_config: GpuConfig | None = None,
+               conv_engine: str = "tc") -> ComputationGraph:
     """CPU-only DAG of a lowered program: demands from each op's launch
     configuration (no profiling; registers 0 and a unit block time unless a GPU
     is present).  Used by CPU tests and to produce reference fixtures."""
@@ -329,7 +368,7 @@ def static_dag(program: Program, gpu_config: GpuConfig | None = None) -> Computa
     for k, op in enumerate(program.ops):
         views = ((0x1000, 0, op.inputs[0].root()[0].shape[-1], op.inputs[0].root()[0].nchw_input),
                  (0x2000, op.output.root()[1], op.output.root()[0].shape[-1]))
-        rec = _op_record(op, views, (0x3000, 0x4000))
+        rec = _op_record(op, views, (0x3000, 0x4000), CONV_ENGINES[conv_engine])
         prof = _lib.OparaOpProfile()
         _lib.check(_lib.lib().opara_op_launch_config(C.byref(rec), C.byref(prof)))
         d = ResourceDemand(prof.threads_per_block, prof.shared_mem_per_block,
