@@ -6,49 +6,59 @@
 //   D[co, p] = sum_k W[co, k] * X[p, k]        co = output channel (UMMA M = 128)
 //                                              p  = output pixel   (UMMA N = BN)
 //                                              k  = (r*S + s)*Cin + c
-// so the accumulator tile lives in TMEM as 128 lanes (channels) x BN columns
-// (pixels) and the epilogue stores 32 consecutive channels of one pixel per
-// warp instruction — coalesced NHWC writes, straight into the concat slice.
+// The accumulator tile lives in TMEM as 128 lanes (channels) x BN columns
+// (pixels).
 //
 // Per CTA (160 threads):
 //   warps 0-3  producers: im2col gather of X with cp.async (16-byte chunks of
-//              4 channels, zero-fill for padding) into the UMMA no-swizzle
-//              K-major core-matrix layout, D=2 stages in flight; then an
-//              in-place split x -> (tf32 hi, tf32 lo); thread 0 also pulls the
-//              pre-packed W hi/lo block of the stage with one bulk async copy
-//              (cp.async.bulk, completion on the stage's mbarrier);
+//              4 channels, zero-fill for padding) straight into the UMMA
+//              no-swizzle K-major core-matrix layout, S-2 stages in flight;
+//              then an in-place split x -> (tf32 hi, tf32 lo).  Thread 0 also
+//              pulls the host-packed W hi/lo block of each stage with one bulk
+//              async copy (cp.async.bulk, completion on the stage mbarrier);
 //   warp 4     MMA issuer (one lane): 3 tcgen05.mma per 8-wide k step
-//              (hi*hi + hi*lo + lo*hi), tcgen05.commit frees the stage;
-//   warps 0-3  epilogue: tcgen05.ld the accumulator, + folded-BN bias, ReLU,
-//              store (or split-K partial + deterministic last-arrival reduce).
-// 4-stage smem ring, full/empty mbarriers, TMEM allocated per CTA.
+//              (hi*hi + hi*lo + lo*hi); tcgen05.commit releases the stage;
+//   epilogue   TMEM -> registers (tcgen05.ld) -> a [BN][128] fp32 tile in the
+//              now idle pipeline smem.
+// Split-K (batch-1 layers are short in M and deep in K) runs as a thread-block
+// cluster along z: every split CTA stages its partial tile in its own smem,
+// one cluster barrier, then CTA rank r reduces rows [r*BN/S, (r+1)*BN/S) by
+// reading that row from every rank over DSMEM in rank order (deterministic),
+// adds the folded-BN bias, applies ReLU and stores 16-byte vectors of 4
+// channels into the output channel view (the concat slice).  No workspace, no
+// atomics, no second kernel.
 
 #include "device_common.cuh"
 #include "ops.h"
 #include "status.h"
 #include "tc_common.cuh"
 
+#include <map>
+#include <mutex>
+
 namespace opara {
 namespace {
 
 constexpr int kBKF = 16;            // k elements (fp32) per stage
-constexpr int kChunks = kBKF / 4;   // 16-byte chunks per row per stage
-constexpr int kStages = 4;
-constexpr int kAhead = 2;           // gather stages in flight per producer thread
-constexpr int kThreads = 160;
+constexpr int kProducerWarps = 8;  // gather + convert; one warp per scheduler is not enough
+constexpr int kMmaWarp = kProducerWarps;      // one elected lane issues tcgen05.mma
+constexpr int kLoadWarp = kProducerWarps + 1;  // one lane streams the packed weights
+constexpr int kThreads = 32 * (kProducerWarps + 2);
+constexpr int kMaxSplits = 8;       // portable cluster size
 constexpr uint32_t kWBytes = 128 * kBKF * 4;  // one precision plane of the W stage
+
+__host__ __device__ constexpr int tc_stages(int bn) { return bn >= 256 ? 4 : 6; }
 
 struct TcArgs {
   const float* __restrict__ in;
   const float* __restrict__ wpack;  // [m_tiles][kblocks][hi|lo][chunk][rg][8][4]
   const float* __restrict__ bias;
   float* __restrict__ out;
-  float* __restrict__ ws;
-  unsigned* __restrict__ cnt;
+  unsigned long long* dbg;          // optional phase timestamps (CTA 0): [warp][8]
   int N, H, W, Cin, in_coff;
   int OH, OW, Cout, out_cs, out_coff;
   int R, S, sh, sw, ph, pw;
-  int relu;
+  int relu, vec_out;
   int M, K, kblocks;
   int splits, kb_per_split;
   int64_t sN, sH, sW, sC;
@@ -66,22 +76,45 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <int BN, bool kVec>
 __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsigned long long* trace) {
+  constexpr int kStages = tc_stages(BN);
   constexpr uint32_t kXBytes = BN * kBKF * 4;
   constexpr uint32_t kStage = 2 * kWBytes + 2 * kXBytes;
-  constexpr uint32_t kLboW = 16 * 128;       // 128 rows = 16 row groups of 128 B
-  constexpr uint32_t kLboX = (BN / 8) * 128;
-  constexpr int kRowsPerThread = BN / 32;    // rows of X each producer thread gathers
+  // Operand planes use the 64-byte-swizzled K-major layout: a row holds the
+  // stage's 16 fp32 k values (64 B = 4 chunks of 16 B), 8-row atoms of 512 B
+  // are stacked along M/N (SBO = 512), and chunk c of row r sits at chunk
+  // position c ^ ((r >> 1) & 3) — bank-conflict-free operand reads for the
+  // tensor core.  An 8-wide k step advances the descriptor start by 32 B.
+  constexpr uint32_t kSbo = 512;
+  constexpr int kRowGroups = BN / 8;
+  constexpr int kRowsPerThread = (kRowGroups + 3) / 4;  // atoms per gather/convert thread
   constexpr uint32_t kIdesc = tc::instr_desc(2, 128, BN);
+  // Separate TMEM accumulators for hi*hi, hi*lo and lo*hi: consecutive MMAs
+  // then target different tiles and overlap in the tensor pipe instead of
+  // serialising on one accumulator (BN = 256 shares one for both corrections).
+  constexpr int kAcc = BN >= 256 ? 2 : 3;
+  constexpr uint32_t kTmemCols = BN >= 256 ? 512 : (BN * 4 <= 32 ? 32 : BN * 4);
+  static_assert(BN * 128 * 4 <= kStages * kStage, "epilogue tile must fit in the pipeline smem");
 
+  // No-swizzle UMMA operands need 16-byte alignment only; indexing the extern
+  // array directly keeps every access in the shared state space (LDS/STS).
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // swizzle atoms must sit on 512-byte boundaries: align the carve-out base
+  // (offsetting the extern array keeps accesses in the shared state space)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
   uint64_t* empty = full + kStages;
-  uint64_t* accum = empty + kStages;
+  uint64_t* landed = empty + kStages;  // gather copies of the stage complete
+  uint64_t* accum = landed + kStages;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(accum + 1);
 
   trace_begin(trace);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool dbg = a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
+#define DBG(slot) \
+  if (dbg) a.dbg[warp * 8 + (slot)] = global_ns();
+  DBG(0);
+  const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (a.dbg && tid == 0 && cta_lin < 96) a.dbg[64 + 2 * cta_lin] = global_ns();
   const int n0 = blockIdx.x * BN;   // first pixel
   const int mt = blockIdx.y;        // 128-channel tile
   const int kb0 = blockIdx.z * a.kb_per_split;
@@ -89,69 +122,89 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      tc::mbar_init(&full[s], 128);
+      tc::mbar_init(&full[s], 32 * (kProducerWarps / 2) + 1);  // converters + the weight loader
+      tc::mbar_init(&landed[s], 32 * (kProducerWarps / 2));   // one noinc arrive per gather thread
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(accum, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 0) tc::tmem_alloc(tslot, BN);
+  if (warp == 0) tc::tmem_alloc(tslot, kTmemCols);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
+  DBG(1);
 
-  if (warp < 4) {
-    // ------------------------------------------------------------ producers
-    const int r8 = lane & 7, cl = lane >> 3;  // row within core matrix, chunk
-    int pb[kRowsPerThread], pih[kRowsPerThread], piw[kRowsPerThread];
-    const int ohw = a.OH * a.OW;
-#pragma unroll
-    for (int j = 0; j < kRowsPerThread; ++j) {
-      const int p = n0 + (warp + 4 * j) * 8 + r8;
-      if (p < a.M) {
-        const int b = p / ohw, rem = p - b * ohw, oh = rem / a.OW, ow = rem - (rem / a.OW) * a.OW;
-        pb[j] = b;
-        pih[j] = oh * a.sh - a.ph;
-        piw[j] = ow * a.sw - a.pw;
-      } else {
-        pb[j] = -1;
-        pih[j] = 0;
-        piw[j] = 0;
-      }
-    }
-    auto x_off = [&](int j) -> uint32_t {  // byte offset of my unit j inside an X plane
-      return static_cast<uint32_t>(cl) * kLboX + static_cast<uint32_t>(warp + 4 * j) * 128u + r8 * 16u;
+  if (warp < kProducerWarps) {
+    // -------------------------------------------- gather (warps 0-3) / convert (4-7)
+    // Warp w and warp w+4 own the same X units: rows of 8-row atoms rw, rw+4, ...
+    // The gather warp streams them into the hi plane with cp.async and the
+    // landed[s] mbarrier fires when its copies complete; the convert warp then
+    // writes lo = x - trunc_tf32(x) and arrives on full[s].  Splitting the
+    // roles lets the gathers run a full ring ahead of the MMA.
+    const bool gather = warp < kProducerWarps / 2;
+    const int rw = warp & 3;
+    const int r8 = lane & 7, cl = lane >> 3;  // row within atom, 16-byte chunk
+    auto x_off = [&](int j) -> uint32_t {     // byte offset of my unit j inside an X plane
+      return static_cast<uint32_t>(rw + 4 * j) * kSbo + r8 * 64u +
+             static_cast<uint32_t>((cl ^ ((r8 >> 1) & 3)) * 16);
     };
-    for (int i = 0; i < nkb + kAhead; ++i) {
-      if (i < nkb) {
+    if (gather) {
+      int pb[kRowsPerThread], pih[kRowsPerThread], piw[kRowsPerThread];
+      const int ohw = a.OH * a.OW;
+#pragma unroll
+      for (int j = 0; j < kRowsPerThread; ++j) {
+        const int p = n0 + (rw + 4 * j) * 8 + r8;
+        if (rw + 4 * j < kRowGroups && p < a.M) {
+          const int b = p / ohw, rem = p - b * ohw, oh = rem / a.OW, ow = rem - oh * a.OW;
+          pb[j] = b;
+          pih[j] = oh * a.sh - a.ph;
+          piw[j] = ow * a.sw - a.pw;
+        } else {
+          pb[j] = -1;
+          pih[j] = 0;
+          piw[j] = 0;
+        }
+      }
+      // vector gather: my 4-channel chunk's k = (r*S + q)*Cin + c, advanced
+      // incrementally by kBKF per stage (no divisions in the loop)
+      const float* rowbase[kRowsPerThread];
+#pragma unroll
+      for (int j = 0; j < kRowsPerThread; ++j)
+        rowbase[j] = a.in + (pb[j] >= 0 ? pb[j] * a.sN + pih[j] * a.sH + piw[j] * a.sW + a.in_coff : 0);
+      int kc = kb0 * kBKF + cl * 4, dc = 0, dr = 0, dq = 0;
+      if (kVec && kc < a.K) {
+        dc = kc % a.Cin;
+        const int rs = kc / a.Cin;
+        dr = rs / a.S;
+        dq = rs - dr * a.S;
+      }
+      for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-        uint8_t* st = smem + s * kStage;
-        if (tid == 0) {
-          tc::mbar_expect_tx(&full[s], 2 * kWBytes);
-          const float* src = a.wpack + (static_cast<int64_t>(mt) * a.kblocks + kb0 + i) * (2 * kWBytes / 4);
-          tc::bulk_g2s(st, src, 2 * kWBytes, &full[s]);
-        }
-        const uint32_t xh = tc::smem_u32(st + 2 * kWBytes);
-        const int kbase = (kb0 + i) * kBKF + cl * 4;
+        if (dbg && tid == 0 && i < 64) a.dbg[768 + i] = global_ns();
+        const uint32_t xh = tc::smem_u32(smem + s * kStage + 2 * kWBytes);
         if constexpr (kVec) {
-          const bool kin = kbase < a.K;
-          int c = 0, r = 0, q = 0;
-          if (kin) {
-            c = kbase % a.Cin;
-            const int rs = kbase / a.Cin;
-            r = rs / a.S;
-            q = rs - r * a.S;
-          }
+          const bool kin = kc < a.K;
+          const int64_t koff = dr * a.sH + dq * a.sW + dc;
 #pragma unroll
           for (int j = 0; j < kRowsPerThread; ++j) {
-            const int ih = pih[j] + r, iw = piw[j] + q;
+            const int ih = pih[j] + dr, iw = piw[j] + dq;
             const bool ok = kin && pb[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
-            const float* src = ok ? a.in + pb[j] * a.sN + ih * a.sH + iw * a.sW + c + a.in_coff : a.in;
-            cp_async16(xh + x_off(j), src, ok);
+            if (rw + 4 * j < kRowGroups) cp_async16(xh + x_off(j), ok ? rowbase[j] + koff : a.in, ok);
+          }
+          kc += kBKF;
+          dc += kBKF;
+          while (dc >= a.Cin) {
+            dc -= a.Cin;
+            if (++dq == a.S) {
+              dq = 0;
+              ++dr;
+            }
           }
         } else {
+          const int kbase = (kb0 + i) * kBKF + cl * 4;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int k = kbase + e;
@@ -168,31 +221,46 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
               const int ih = pih[j] + r, iw = piw[j] + q;
               const bool ok = kin && pb[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
               const float* src = ok ? a.in + pb[j] * a.sN + ih * a.sH + iw * a.sW + c * a.sC + a.in_coff : a.in;
-              cp_async4(xh + x_off(j) + 4 * e, src, ok);
+              if (rw + 4 * j < kRowGroups) cp_async4(xh + x_off(j) + 4 * e, src, ok);
             }
           }
         }
+        tc::cp_async_arrive_noinc(&landed[s]);
       }
-      cp_async_commit();
-      const int jst = i - kAhead;
-      if (jst >= 0) {
-        cp_async_wait<kAhead>();
-        const int s = jst % kStages;
+    } else {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        tc::mbar_wait(&landed[s], (i / kStages) & 1);
+        if (dbg && warp == 4 && lane == 0 && i < 64) a.dbg[256 + i] = global_ns();
         uint8_t* xh = smem + s * kStage + 2 * kWBytes;
         uint8_t* xl = xh + kXBytes;
 #pragma unroll
         for (int j = 0; j < kRowsPerThread; ++j) {
-          float4* ph = reinterpret_cast<float4*>(xh + x_off(j));
-          float4 v = *ph, hi, lo;
-          hi.x = tc::to_tf32(v.x); lo.x = tc::to_tf32(v.x - hi.x);
-          hi.y = tc::to_tf32(v.y); lo.y = tc::to_tf32(v.y - hi.y);
-          hi.z = tc::to_tf32(v.z); lo.z = tc::to_tf32(v.z - hi.z);
-          hi.w = tc::to_tf32(v.w); lo.w = tc::to_tf32(v.w - hi.w);
-          *ph = hi;
+          if (rw + 4 * j >= kRowGroups) break;
+          // The tensor core reads an fp32 operand as tf32 by dropping the low
+          // 13 mantissa bits, so the raw x already serves as the hi plane;
+          // only lo = x - trunc_tf32(x) (exact in fp32) is materialised.
+          const float4 v = *reinterpret_cast<const float4*>(xh + x_off(j));
+          float4 lo;
+          lo.x = v.x - tc::trunc_tf32(v.x);
+          lo.y = v.y - tc::trunc_tf32(v.y);
+          lo.z = v.z - tc::trunc_tf32(v.z);
+          lo.w = v.w - tc::trunc_tf32(v.w);
           *reinterpret_cast<float4*>(xl + x_off(j)) = lo;
         }
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(&full[s]);
+      }
+    }
+  } else if (warp == kLoadWarp) {
+    // ------------------------------------------------------------ weight loader
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&full[s], 2 * kWBytes);
+        const float* src = a.wpack + (static_cast<int64_t>(mt) * a.kblocks + kb0 + i) * (2 * kWBytes / 4);
+        tc::bulk_g2s(smem + s * kStage, src, 2 * kWBytes, &full[s]);
       }
     }
   } else if (lane == 0) {
@@ -201,92 +269,129 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       const int s = i % kStages;
       tc::mbar_wait(&full[s], (i / kStages) & 1);
       tc::tc_fence_after();
+      if (dbg && i < 64) a.dbg[512 + i] = global_ns();
       const uint32_t base = tc::smem_u32(smem + s * kStage);
       const uint32_t w_hi = base, w_lo = base + kWBytes;
       const uint32_t x_hi = base + 2 * kWBytes, x_lo = x_hi + kXBytes;
 #pragma unroll
       for (int ks = 0; ks < kBKF / 8; ++ks) {
-        const uint64_t ah = tc::smem_desc(w_hi + 2 * ks * kLboW, kLboW, 128);
-        const uint64_t al = tc::smem_desc(w_lo + 2 * ks * kLboW, kLboW, 128);
-        const uint64_t bh = tc::smem_desc(x_hi + 2 * ks * kLboX, kLboX, 128);
-        const uint64_t bl = tc::smem_desc(x_lo + 2 * ks * kLboX, kLboX, 128);
-        tc::mma_tf32(tmem, ah, bh, kIdesc, (i | ks) != 0);
-        tc::mma_tf32(tmem, ah, bl, kIdesc, 1);
-        tc::mma_tf32(tmem, al, bh, kIdesc, 1);
+        const uint64_t ah = tc::smem_desc_sw64(w_hi + 32 * ks, kSbo);
+        const uint64_t al = tc::smem_desc_sw64(w_lo + 32 * ks, kSbo);
+        const uint64_t bh = tc::smem_desc_sw64(x_hi + 32 * ks, kSbo);
+        const uint64_t bl = tc::smem_desc_sw64(x_lo + 32 * ks, kSbo);
+        const uint32_t first = (i | ks) != 0;
+        tc::mma_tf32(tmem, ah, bh, kIdesc, first);
+        tc::mma_tf32(tmem + BN, ah, bl, kIdesc, first);
+        tc::mma_tf32(tmem + (kAcc - 1) * BN, al, bh, kIdesc, kAcc == 3 ? first : 1u);
       }
       tc::mma_commit(&empty[s]);
     }
     tc::mma_commit(accum);
+    DBG(2);
   }
   __syncwarp();
 
-  // ---------------------------------------------------------------- epilogue
-  const int ch = mt * 128 + warp * 32 + lane;
-  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-  const int64_t plane = static_cast<int64_t>(a.M) * a.Cout;
-  bool do_final = true;
-  if (a.splits > 1) {
-    if (warp < 4) {
-      tc::mbar_wait(accum, 0);
-      tc::tc_fence_after();
-      float* mine = a.ws + blockIdx.z * plane;
-#pragma unroll 1
-      for (int c8 = 0; c8 < BN / 8; ++c8) {
-        float v[8];
-        tc::tmem_ld8(trow + c8 * 8, v);
-        if (ch < a.Cout) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int p = n0 + c8 * 8 + e;
-            if (p < a.M) __stcg(mine + static_cast<int64_t>(p) * a.Cout + ch, v[e]);
-          }
-        }
-      }
-    }
-    do_final = splitk_arrive_last(a.cnt + blockIdx.x + blockIdx.y * gridDim.x, a.splits);
-    if (do_final && warp < 4 && ch < a.Cout) {
-      const float bias = a.bias ? __ldg(a.bias + ch) : 0.f;
-      for (int p = n0; p < min(n0 + BN, a.M); ++p) {
-        float s = 0.f;
-        for (int z = 0; z < a.splits; ++z) s += __ldcg(a.ws + z * plane + static_cast<int64_t>(p) * a.Cout + ch);
-        s += bias;
-        if (a.relu) s = fmaxf(s, 0.f);
-        a.out[static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch] = s;
-      }
-    }
-  } else if (warp < 4) {
+  // ------------------------------------------------------------ epilogue
+  // TMEM -> [BN][128] fp32 tile in the idle pipeline smem (all MMAs, hence all
+  // smem reads by the tensor core, are complete once `accum` fires).
+  DBG(3);
+  float* tile = reinterpret_cast<float*>(smem);
+  if (warp < kProducerWarps) {
+    // warp w may only touch TMEM lanes [32*(w%4), +32): lane quarter w%4,
+    // column half w/4
     tc::mbar_wait(accum, 0);
     tc::tc_fence_after();
-    const float bias = (ch < a.Cout && a.bias) ? __ldg(a.bias + ch) : 0.f;
-#pragma unroll 1
-    for (int c8 = 0; c8 < BN / 8; ++c8) {
+    DBG(4);
+    const int quarter = warp & 3, half = warp >> 2;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    constexpr int kC8 = BN / 8 / (kProducerWarps / 4);
+#pragma unroll 4
+    for (int c8 = half * kC8; c8 < (half + 1) * kC8; ++c8) {
       float v[8];
       tc::tmem_ld8(trow + c8 * 8, v);
-      if (ch < a.Cout) {
+      {
+        float c1[8], c2[8];
+        tc::tmem_ld8(trow + BN + c8 * 8, c1);
+        if constexpr (kAcc == 3) tc::tmem_ld8(trow + 2 * BN + c8 * 8, c2);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int p = n0 + c8 * 8 + e;
-          if (p < a.M) {
-            float y = v[e] + bias;
-            if (a.relu) y = fmaxf(y, 0.f);
-            a.out[static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch] = y;
-          }
-        }
+        for (int e = 0; e < 8; ++e) v[e] += kAcc == 3 ? (c1[e] + c2[e]) : c1[e];
       }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) tile[(c8 * 8 + e) * 128 + quarter * 32 + lane] = v[e];
     }
   }
   tc::tc_fence_before();
-  __syncthreads();
+  const int splits = a.splits;
+  if (splits > 1)
+    tc::cluster_sync();
+  else
+    __syncthreads();
+  DBG(5);
+  // rows [r0, r1) of the tile are reduced (over the cluster) and stored by this CTA
+  const int rank = splits > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
+  const int rows_per = (BN + splits - 1) / splits;
+  const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
+  const int ch = mt * 128 + lane * 4;
+  float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (a.bias) {
+    if (ch + 0 < a.Cout) bias4.x = __ldg(a.bias + ch + 0);
+    if (ch + 1 < a.Cout) bias4.y = __ldg(a.bias + ch + 1);
+    if (ch + 2 < a.Cout) bias4.z = __ldg(a.bias + ch + 2);
+    if (ch + 3 < a.Cout) bias4.w = __ldg(a.bias + ch + 3);
+  }
+  const uint32_t tile_s = tc::smem_u32(tile);
+  for (int row = r0 + warp; row < r1; row += kThreads / 32) {
+    const int p = n0 + row;
+    if (p >= a.M) break;
+    const uint32_t off = static_cast<uint32_t>((row * 128 + lane * 4) * 4);
+    float4 acc;
+    if (splits > 1) {
+      // issue every rank's load first (independent DSMEM round trips), then
+      // add in rank order so the result does not depend on timing
+      float4 part[kMaxSplits];
+#pragma unroll
+      for (int z = 0; z < kMaxSplits; ++z)
+        if (z < splits) part[z] = tc::ld_dsmem_f4(tc::map_cluster(tile_s + off, z));
+      acc = part[0];
+#pragma unroll
+      for (int z = 1; z < kMaxSplits; ++z)
+        if (z < splits) {
+          acc.x += part[z].x; acc.y += part[z].y; acc.z += part[z].z; acc.w += part[z].w;
+        }
+    } else {
+      acc = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(tile) + off);
+    }
+    acc.x += bias4.x; acc.y += bias4.y; acc.z += bias4.z; acc.w += bias4.w;
+    if (a.relu) {
+      acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f);
+      acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
+    }
+    float* dst = a.out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
+    if (a.vec_out && ch + 3 < a.Cout) {
+      *reinterpret_cast<float4*>(dst) = acc;
+    } else {
+      if (ch + 0 < a.Cout) dst[0] = acc.x;
+      if (ch + 1 < a.Cout) dst[1] = acc.y;
+      if (ch + 2 < a.Cout) dst[2] = acc.z;
+      if (ch + 3 < a.Cout) dst[3] = acc.w;
+    }
+  }
+  DBG(6);
+  if (splits > 1) tc::cluster_sync();  // peers may still be reading this CTA's tile
+  else __syncthreads();
   if (warp == 0) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, BN);
+    tc::tmem_dealloc(tmem, kTmemCols);
   }
+  DBG(7);
+  if (a.dbg && tid == 0 && cta_lin < 96) a.dbg[64 + 2 * cta_lin + 1] = global_ns();
+#undef DBG
   trace_end(trace);
 }
 
 template <int BN>
 constexpr size_t tc_smem_bytes() {
-  return kStages * (2 * kWBytes + 2 * static_cast<size_t>(BN) * kBKF * 4) + 256 + 1024;
+  return tc_stages(BN) * (2 * kWBytes + 2 * static_cast<size_t>(BN) * kBKF * 4) + 512 + 1024;
 }
 
 struct TcVariant {
@@ -322,6 +427,71 @@ opara_status set_smem_attr(const TcVariant& v) {
   return OPARA_OK;
 }
 
+// How many clusters of `size` CTAs fit on the device at once (cached per
+// kernel/size; without a device assume the 148-SM / one-CTA-per-SM bound).
+int64_t max_active_clusters(const void* func, int size, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int64_t> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(func, size);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int64_t result = 148 / size;
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0 &&
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) ==
+          cudaSuccess) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(1, 1, size);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = size;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, func, &lc) == cudaSuccess && n > 0) result = n;
+  }
+  cudaGetLastError();
+  cache[key] = result;
+  return result;
+}
+
+// Tile/split choice: pixel tile BN and split count so one conv spreads over
+// about `target` CTAs (clusters of <= 8 splits), keeping >= 2 k-blocks each.
+void choose_tiling(const TcArgs& a, int64_t target, int forced_bn, int forced_splits, int* bn_id,
+                   int* splits) {
+  const int mtiles = (a.Cout + 127) / 128;
+  int id = forced_bn;
+  if (id < 0) {
+    // largest tile that still gives >= 32 output tiles, else the smallest
+    id = 0;
+    const int bns[4] = {32, 64, 128, 256};
+    for (int k = 3; k >= 0; --k) {
+      const int64_t tiles = static_cast<int64_t>((a.M + bns[k] - 1) / bns[k]) * mtiles;
+      if (tiles >= 32 || k == 0) {
+        id = k;
+        break;
+      }
+    }
+    // pixel counts just above a tile multiple waste a whole tile: step down
+    if (id > 0 && a.M < 64 * 2) id = a.M > 32 ? 1 : 0;
+  }
+  const int bn = 32 << id;
+  const int64_t base = static_cast<int64_t>((a.M + bn - 1) / bn) * mtiles;
+  // one CTA per SM (the pipeline uses most of the 228 KB): stay within one
+  // wave of 148 CTAs, a second wave would double the latency
+  int64_t s = forced_splits > 0 ? forced_splits : std::max<int64_t>(1, target / base);
+  s = std::min<int64_t>(s, kMaxSplits);
+  s = std::min<int64_t>(s, std::max(1, a.kblocks / 2));
+  s = std::max<int64_t>(1, s);
+  *bn_id = id;
+  *splits = static_cast<int>(s);
+}
+
 }  // namespace
 
 // CONV2D with i[22] == 1 (engine "tc"): weights in p[1] are pre-packed by the
@@ -333,6 +503,7 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   a.wpack = static_cast<const float*>(op.p[1]);
   a.bias = static_cast<const float*>(op.p[2]);
   a.out = static_cast<float*>(op.p[3]);
+  a.dbg = static_cast<unsigned long long*>(op.p[6]);
   a.N = (int)op.i[0]; a.H = (int)op.i[1]; a.W = (int)op.i[2]; a.Cin = (int)op.i[3];
   const int in_cs = (int)op.i[4];
   a.in_coff = (int)op.i[5];
@@ -360,38 +531,47 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   if (a.M <= 0 || a.Cout <= 0 || a.K <= 0) return fail(OPARA_ERR_VALUE, "conv2d: empty shape");
   const bool vec = !nchw && a.Cin % 4 == 0 && in_cs % 4 == 0 && a.in_coff % 4 == 0 &&
                    reinterpret_cast<uintptr_t>(a.in) % 16 == 0;
+  a.vec_out = (a.out_cs % 4 == 0 && a.out_coff % 4 == 0 && reinterpret_cast<uintptr_t>(a.out) % 16 == 0) ? 1 : 0;
   int count = 0;
   const TcVariant* v = tc_variants(&count);
-  int id = op.variant;
-  if (id < 0 || id >= count) id = a.M >= 2048 ? 2 : (a.M > 96 ? 1 : (a.M > 32 ? 1 : 0));
-  const int mtiles = (a.Cout + 127) / 128;
-  const int64_t base = static_cast<int64_t>((a.M + v[id].bn - 1) / v[id].bn) * mtiles;
+  int id = 0, splits = 1;
   const int64_t target = op.i[21] > 0 ? op.i[21] : 148;
-  int64_t splits = op.i[19] > 1 ? op.i[19] : std::max<int64_t>(1, target / std::max<int64_t>(1, base));
-  splits = std::min<int64_t>(splits, std::max(1, a.kblocks / 3));
-  a.kb_per_split = static_cast<int>((a.kblocks + splits - 1) / splits);
+  choose_tiling(a, target, (op.variant >= 0 && op.variant < count) ? op.variant : -1,
+                op.i[19] > 1 ? static_cast<int>(op.i[19]) : 0, &id, &splits);
+  const void* func = v[id].func[vec ? 1 : 0];
+  if (splits > 1 && op.i[19] <= 1) {
+    // clusters must be co-resident inside a GPC: keep every cluster in the
+    // first wave (a second wave doubles the latency of the whole conv)
+    const int64_t clusters = static_cast<int64_t>((a.M + v[id].bn - 1) / v[id].bn) * ((a.Cout + 127) / 128);
+    while (splits > 1 && clusters > max_active_clusters(func, splits, v[id].smem)) --splits;
+  }
+  a.kb_per_split = (a.kblocks + splits - 1) / splits;
   a.splits = (a.kblocks + a.kb_per_split - 1) / a.kb_per_split;
   LaunchCfg c;
-  c.func = v[id].func[vec ? 1 : 0];
-  c.grid = dim3(ceil_div(a.M, v[id].bn), mtiles, a.splits);
+  c.func = func;
+  c.grid = dim3(ceil_div(a.M, v[id].bn), (a.Cout + 127) / 128, a.splits);
   c.block = dim3(kThreads);
   c.smem = v[id].smem;
-  const int64_t tiles = static_cast<int64_t>(c.grid.x) * c.grid.y;
-  c.workspace = a.splits > 1 ? splitk_workspace_bytes(static_cast<int64_t>(a.M) * a.Cout * a.splits, tiles) : 0;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
   opara_status st = set_smem_attr(v[id]);
   if (st != OPARA_OK) return st;
-  if (a.splits > 1) {
-    if (!op.p[7]) return fail(OPARA_ERR_INTERNAL, "conv2d_tc: split-K workspace missing");
-    a.ws = static_cast<float*>(op.p[7]);
-    a.cnt = splitk_counters(op.p[7], static_cast<int64_t>(a.M) * a.Cout * a.splits);
-  } else {
-    a.ws = nullptr;
-    a.cnt = nullptr;
-  }
   void* args[] = {&a, &trace};
-  return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, c.smem, s), "conv2d_tc launch");
+  if (a.splits == 1)
+    return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, c.smem, s), "conv2d_tc launch");
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = c.grid;
+  lc.blockDim = c.block;
+  lc.dynamicSmemBytes = c.smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = a.splits;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  return cuda_fail(cudaLaunchKernelExC(&lc, c.func, args), "conv2d_tc cluster launch");
 }
 
 }  // namespace opara

@@ -60,6 +60,18 @@ def block_duration_us(isolated_us: float, d: ResourceDemand, cfg: GpuConfig) -> 
 CONV_ENGINES = {"simt": 0, "tc": 1}
 
 
+def conv_engine_for(op, requested: int) -> int:
+    """Per-conv engine: the tensor-core kernel gathers 16-byte chunks of 4
+    channels, so convs over the raw NCHW graph input or with Cin % 4 != 0 (the
+    3-channel stems) run on the exact-fp32 SIMT kernel."""
+    if op.kind != CONV2D or requested != 1:
+        return requested
+    x = op.inputs[0].root()[0]
+    if x.nchw_input or op.ints["Cin"] % 4 != 0:
+        return 0
+    return 1
+
+
 def tf32_rna(x: np.ndarray) -> np.ndarray:
     """fp32 -> tf32 round-to-nearest, ties away (cvt.rna.tf32.f32), as fp32."""
     b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
@@ -73,18 +85,25 @@ def pack_conv_weights_tf32x3(wk: np.ndarray) -> np.ndarray:
     Rows = output channels (UMMA M, padded to 128-row tiles), columns = k
     (padded to 16-element blocks).  Every (m-tile, k-block) becomes one
     contiguous 16 KiB record: the tf32 hi plane then the tf32 lo plane, each in
-    the no-swizzle K-major core-matrix order [chunk(4)][row group(16)][row(8)]
-    [4 fp32] that conv_tc.cu's smem descriptors (LBO 2048 B, SBO 128 B) expect.
+    the 64-byte-swizzled K-major order [atom(16)][row(8)][chunk(4), XOR-permuted
+    by (row >> 1) & 3][4 fp32] that conv_tc.cu's SWIZZLE_64B descriptors expect.
     """
     k, cout = wk.shape
     mt, kb = -(-cout // 128), -(-k // 16)
     w = np.zeros((mt * 128, kb * 16), dtype=np.float32)
     w[:cout, :k] = wk.T
     hi = tf32_rna(w)
-    lo = tf32_rna(w - hi)
+    lo = tf32_rna(w - hi)  # hi/lo exact tf32 values: the hardware truncation is a no-op on them
+
+    # 64-byte swizzle: chunk c of row r (r = row % 8) lands at chunk c ^ ((r >> 1) & 3)
+    r = np.arange(8)[:, None]
+    c = np.arange(4)[None, :]
+    perm = c ^ ((r >> 1) & 3)          # destination chunk of source chunk c in row r
+    inv = np.argsort(perm, axis=1)     # source chunk stored at destination chunk
 
     def image(x):
-        return x.reshape(mt, 16, 8, kb, 4, 4).transpose(0, 3, 4, 1, 2, 5)
+        t = x.reshape(mt, 16, 8, kb, 4, 4).transpose(0, 3, 1, 2, 4, 5)  # (mt, kb, atom, r, chunk, e)
+        return np.take_along_axis(t, inv[None, None, None, :, :, None], axis=4)
 
     return np.ascontiguousarray(np.stack([image(hi), image(lo)], axis=2)).reshape(-1)
 
@@ -146,7 +165,15 @@ class ScheduledGraph:
         self._alloc(program)
         recs = (_lib.OparaOp * len(program.ops))()
         for k, op in enumerate(program.ops):
-            recs[k] = _op_record(op, self._views(op), self._weights(op), self.conv_engine)
+            recs[k] = _op_record(op, self._views(op), self._weights(op),
+                                 conv_engine_for(op, self.conv_engine))
+        self.debug_ts = {}
+        if os.environ.get("OPARA_CONV_DEBUG"):  # per-phase timestamps of CTA 0 (conv_tc.cu)
+            for k, op in enumerate(program.ops):
+                if op.kind == CONV2D:
+                    buf = torch.zeros(4096 + 64, dtype=torch.int64, device=self.dev)
+                    self.debug_ts[k] = buf
+                    recs[k].p[6] = buf.data_ptr()
         self._recs = recs
         L = _lib.lib()
         h = C.c_void_p()
@@ -193,7 +220,7 @@ class ScheduledGraph:
     def _weights(self, op):
         ptrs = []
         weight = op.weight
-        if op.kind == CONV2D and self.conv_engine == 1:
+        if op.kind == CONV2D and conv_engine_for(op, self.conv_engine) == 1:
             weight = pack_conv_weights_tf32x3(op.weight)
         for arr in (weight, op.bias):
             if arr is None:
@@ -368,7 +395,7 @@ def static_dag(program: Program, gpu_config: GpuConfig | None = None,
     for k, op in enumerate(program.ops):
         views = ((0x1000, 0, op.inputs[0].root()[0].shape[-1], op.inputs[0].root()[0].nchw_input),
                  (0x2000, op.output.root()[1], op.output.root()[0].shape[-1]))
-        rec = _op_record(op, views, (0x3000, 0x4000), CONV_ENGINES[conv_engine])
+        rec = _op_record(op, views, (0x3000, 0x4000), conv_engine_for(op, CONV_ENGINES[conv_engine]))
         prof = _lib.OparaOpProfile()
         _lib.check(_lib.lib().opara_op_launch_config(C.byref(rec), C.byref(prof)))
         d = ResourceDemand(prof.threads_per_block, prof.shared_mem_per_block,

@@ -1,9 +1,9 @@
-# build -> GPU kernel tests -> smoke -> bench (googlenet + inception_v3)
-set -x
+# build -> GPU kernel tests -> smoke -> bench (googlenet + inception_v3) -> per-op profile
 python __graft_entry__.py || exit 1
-timeout 900 python -m pytest tests/test_gpu_kernels.py -x -q 2>&1 | tail -15
+timeout 900 python -m pytest tests/test_gpu_kernels.py -x -q 2>&1 | tail -3
 timeout 600 python __graft_entry__.py smoke 2>&1 | tail -3
 for m in googlenet inception_v3; do
   timeout 900 python bench.py --model $m --steps 100 --warmup 10 --cpu-seconds 2 > gpurun_out/bench_$m.json 2> gpurun_out/bench_$m.err
-  python -c "import json;d=json.load(open('gpurun_out/bench_$m.json'));print('$m', 'lat',d['latency_ms'],'seq',d['sequential_latency_ms'],'x',d['speedup_vs_sequential'],'cp',d['dag_roofline']['critical_path_us'],'frac',d['dag_roofline']['frac'],'conv TF',d['roofline']['achieved'],'rel',d['rel_err_vs_torch_fp32'])"
+  python -c "import json;d=json.load(open('gpurun_out/bench_$m.json'));print('$m', 'lat',d['latency_ms'],'seq',d['sequential_latency_ms'],'x',d['speedup_vs_sequential'],'cp',d['dag_roofline']['critical_path_us'],'frac',d['dag_roofline']['frac'],'conv TF',d['roofline']['achieved'],'rel',d['rel_err_vs_torch_fp32'])" || tail -5 gpurun_out/bench_$m.err
+  timeout 600 python scripts/profile_ops.py $m
 done

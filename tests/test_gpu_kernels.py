@@ -82,7 +82,8 @@ def test_conv_matches_torch(case, engine_name):
         ref = m.double()(x.double())
     y_nchw = y.permute(0, 3, 1, 2).cpu()
     assert y_nchw.shape == ref.shape
-    assert _rel(y_nchw, ref) < 2e-6
+    # 3xTF32 drops the lo*lo term: ~1e-6 over K ~ 2.6k; exact-fp32 SIMT ~3e-7
+    assert _rel(y_nchw, ref) < (1e-5 if engine_name == "tc" else 2e-6)
     # replaying twice is idempotent (split-K counters reset themselves)
     y2 = sg.run(x.cuda())
     assert torch.equal(y, y2)
