@@ -163,7 +163,7 @@ def run_gpu(args) -> dict | None:
     from paper_2312_10351_b200.dag import graph_to_dict
 
     model, x = zoo.build(args.model)
-    sg = engine.compile(model, x, device=local)
+    sg = engine.compile(model, x, device=local, bound_grids=args.bounded)
     xd = x.cuda(local)
     # correctness guard on every rank: a fast wrong answer is not a result
     y = sg.run(xd)
@@ -358,6 +358,9 @@ def main(argv=None) -> int:
     ap.add_argument("--model", default="inception_v3", choices=["inception_v3", "googlenet"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--bounded", action="store_true",
+                    help="size each conv for its DAG level's share of the SMs (Opara bounded grids) "
+                         "instead of the whole GPU")
     args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
     line = run_reference(args) if args.impl == "reference" else run_gpu(args)

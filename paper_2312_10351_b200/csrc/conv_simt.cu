@@ -51,6 +51,8 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   __shared__ __align__(16) float As[2][BK][BM + 4];
   __shared__ __align__(16) float Bs[2][BK][BN + 4];
   trace_begin(trace);
+  pdl_trigger();
+  pdl_wait();
 
   const int tid = threadIdx.x;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -330,7 +332,7 @@ opara_status launch_conv2d(const opara_op& op, cudaStream_t s, unsigned long lon
     a.cnt = nullptr;
   }
   void* args[] = {&a, &trace};
-  return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, c.smem, s), "conv2d launch");
+  return launch_kernel(c, args, s);
 }
 
 }  // namespace opara

@@ -47,7 +47,9 @@ constexpr int kThreads = 32 * (kProducerWarps + 2);
 constexpr int kMaxSplits = 8;       // portable cluster size
 constexpr uint32_t kWBytes = 128 * kBKF * 4;  // one precision plane of the W stage
 
-__host__ __device__ constexpr int tc_stages(int bn) { return bn >= 256 ? 4 : 6; }
+// Ring depth per pixel tile: the small tiles keep the CTA under ~113 KB so two
+// CTAs (two concurrent branches) can share an SM.
+__host__ __device__ constexpr int tc_stages(int bn) { return bn == 32 ? 5 : bn == 64 ? 4 : bn == 128 ? 6 : 4; }
 
 struct TcArgs {
   const float* __restrict__ in;
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   uint32_t* tslot = reinterpret_cast<uint32_t*>(accum + 1);
 
   trace_begin(trace);
+  pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool dbg = a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
 #define DBG(slot) \
@@ -180,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
         dr = rs / a.S;
         dq = rs - dr * a.S;
       }
+      pdl_wait();  // the input activations come from the predecessor grid
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
@@ -557,21 +561,7 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   opara_status st = set_smem_attr(v[id]);
   if (st != OPARA_OK) return st;
   void* args[] = {&a, &trace};
-  if (a.splits == 1)
-    return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, c.smem, s), "conv2d_tc launch");
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = c.grid;
-  lc.blockDim = c.block;
-  lc.dynamicSmemBytes = c.smem;
-  lc.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = a.splits;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  return cuda_fail(cudaLaunchKernelExC(&lc, c.func, args), "conv2d_tc cluster launch");
+  return launch_kernel(c, args, s, a.splits > 1 ? static_cast<unsigned>(a.splits) : 1u);
 }
 
 }  // namespace opara

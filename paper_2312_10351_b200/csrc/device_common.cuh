@@ -42,6 +42,12 @@ __device__ __forceinline__ bool splitk_arrive_last(unsigned* cnt, int splits) {
   return last;
 }
 
+// Programmatic dependent launch: let the next kernel of the stream start its
+// prologue now, and wait (before touching predecessor outputs) until every
+// predecessor grid has completed and flushed its memory.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -26,6 +27,39 @@ opara_status cuda_fail(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return OPARA_OK;
   return fail(OPARA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" +
                                   cudaGetErrorString(e) + ")");
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("OPARA_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+opara_status launch_kernel(const LaunchCfg& c, void** args, cudaStream_t s, unsigned cluster_z) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = c.grid;
+  lc.blockDim = c.block;
+  lc.dynamicSmemBytes = c.smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_z > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = 1;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = cluster_z;
+    ++n;
+  }
+  lc.attrs = attr;
+  lc.numAttrs = n;
+  return cuda_fail(cudaLaunchKernelExC(&lc, c.func, args), "kernel launch");
 }
 
 opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* trace,

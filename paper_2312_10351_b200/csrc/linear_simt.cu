@@ -31,6 +31,8 @@ __device__ __forceinline__ float activate(float v, int act) {
 template <int kRows, bool kVec>
 __global__ void __launch_bounds__(256) linear_rows_f32(LinArgs a, unsigned long long* trace) {
   trace_begin(trace);
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warps_per_block = blockDim.x / 32;
   const int row_groups = (a.M + kRows - 1) / kRows;
@@ -110,7 +112,7 @@ opara_status launch_linear(const opara_op& op, cudaStream_t s, unsigned long lon
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
   void* args[] = {&a, &trace};
-  return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, 0, s), "linear launch");
+  return launch_kernel(c, args, s);
 }
 
 }  // namespace opara

@@ -69,6 +69,15 @@ opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* t
 
 opara_status cuda_fail(cudaError_t e, const char* what);
 
+// Launch `cfg` on `s` with programmatic dependent launch (PDL) enabled, and as
+// a (1, 1, cluster_z) thread-block cluster when cluster_z > 1.  Every kernel
+// of the executor starts with griddepcontrol.launch_dependents and executes
+// griddepcontrol.wait before its first read of a predecessor's output, so a
+// same-stream successor's prologue (barrier init, TMEM alloc, weight
+// prefetch) overlaps this kernel's tail inside the captured graph.
+opara_status launch_kernel(const LaunchCfg& cfg, void** args, cudaStream_t s, unsigned cluster_z = 1);
+bool pdl_enabled();
+
 inline unsigned ceil_div(int64_t a, int64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
 }  // namespace opara

@@ -23,6 +23,8 @@ struct PoolArgs {
 template <bool kMax, int V>
 __global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long long* trace) {
   trace_begin(trace);
+  pdl_trigger();
+  pdl_wait();
   const int cv = a.C / V;
   const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -87,6 +89,8 @@ __global__ void __launch_bounds__(256) global_avgpool_nhwc(const float* __restri
                                                            int C, int in_cs, int in_coff,
                                                            unsigned long long* trace) {
   trace_begin(trace);
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
   const int64_t total = static_cast<int64_t>(N) * C;
@@ -111,6 +115,8 @@ __global__ void __launch_bounds__(128) global_avgpool_nhwc_cols(const float* __r
                                                                 int in_coff,
                                                                 unsigned long long* trace) {
   trace_begin(trace);
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = static_cast<int64_t>(N) * C;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -156,7 +162,7 @@ opara_status launch_pool2d(const opara_op& op, cudaStream_t s, unsigned long lon
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
   void* args[] = {&a, &trace};
-  return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, 0, s), "pool2d launch");
+  return launch_kernel(c, args, s);
 }
 
 opara_status launch_global_avgpool(const opara_op& op, cudaStream_t s, unsigned long long* trace,
@@ -181,7 +187,7 @@ opara_status launch_global_avgpool(const opara_op& op, cudaStream_t s, unsigned 
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
   void* args[] = {&in, &out, &N, &HW, &C, &in_cs, &in_coff, &trace};
-  return cuda_fail(cudaLaunchKernel(c.func, c.grid, c.block, args, 0, s), "global_avgpool launch");
+  return launch_kernel(c, args, s);
 }
 
 }  // namespace opara

@@ -108,7 +108,30 @@ def pack_conv_weights_tf32x3(wk: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(np.stack([image(hi), image(lo)], axis=2)).reshape(-1)
 
 
-def _op_record(op, views, weights, conv_engine: int = 1) -> _lib.OparaOp:
+def concurrency_targets(program: Program, num_sms: int = 148) -> dict[int, int]:
+    """CTA budget per conv: the SMs are shared among the convs of the same DAG
+    level (longest-path depth) in proportion to their FLOPs, so branches that
+    can run concurrently are sized to co-reside instead of each claiming the
+    whole GPU (Opara's bounded grids)."""
+    n = len(program.ops)
+    preds = [[] for _ in range(n)]
+    for u, v in program.edges:
+        preds[v].append(u)
+    level = [0] * n
+    for v in range(n):  # ops are emitted in topological order
+        level[v] = 1 + max((level[u] for u in preds[v]), default=-1)
+    work: dict[int, int] = {}
+    for v, op in enumerate(program.ops):
+        if op.kind == CONV2D:
+            work[level[v]] = work.get(level[v], 0) + op.flops
+    out = {}
+    for v, op in enumerate(program.ops):
+        if op.kind == CONV2D and work.get(level[v]):
+            out[v] = max(8, int(round(num_sms * op.flops / work[level[v]])))
+    return out
+
+
+def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -> _lib.OparaOp:
     """Fill the POD launch record of one lowered op (layouts: csrc/ops.h)."""
     rec = _lib.OparaOp()
     rec.kind = op.kind
@@ -120,8 +143,8 @@ def _op_record(op, views, weights, conv_engine: int = 1) -> _lib.OparaOp:
     i = rec.i
     if op.kind == CONV2D:
         vals = [q["N"], q["H"], q["W"], q["Cin"], ics, icoff, q["OH"], q["OW"], q["Cout"], ocs, ocoff,
-                q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], 0, 1, int(inchw), 0,
-                conv_engine]
+                q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], 0, 1, int(inchw),
+                int(target_ctas), conv_engine]
         rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
     elif op.kind in (MAXPOOL2D, AVGPOOL2D):
         vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff, q["OH"], q["OW"], ocs, ocoff, q["kh"],
@@ -153,7 +176,7 @@ class ScheduledGraph:
 
     def __init__(self, program: Program, device: int, policy: str = "opara",
                  gpu_config: GpuConfig | None = None, profile_reps: int = 20, seed: int | None = None,
-                 conv_engine: str = "tc"):
+                 conv_engine: str = "tc", bound_grids: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("ScheduledGraph needs a CUDA device (there is no CPU fallback)")
         self.program = program
@@ -164,9 +187,10 @@ class ScheduledGraph:
         self._keep: list[torch.Tensor] = []
         self._alloc(program)
         recs = (_lib.OparaOp * len(program.ops))()
+        self.targets = concurrency_targets(program) if bound_grids else {}
         for k, op in enumerate(program.ops):
             recs[k] = _op_record(op, self._views(op), self._weights(op),
-                                 conv_engine_for(op, self.conv_engine))
+                                 conv_engine_for(op, self.conv_engine), self.targets.get(k, 0))
         self.debug_ts = {}
         if os.environ.get("OPARA_CONV_DEBUG"):  # per-phase timestamps of CTA 0 (conv_tc.cu)
             for k, op in enumerate(program.ops):
@@ -377,25 +401,29 @@ class ScheduledGraph:
 
 def compile(model: torch.nn.Module, example: torch.Tensor, *, device: int = 0, policy: str = "opara",
             gpu_config: GpuConfig | None = None, profile_reps: int = 20,
-            seed: int | None = None, conv_engine: str = "tc") -> ScheduledGraph:
+            seed: int | None = None, conv_engine: str = "tc",
+            bound_grids: bool = False) -> ScheduledGraph:
     """Model in, scheduled graph out."""
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     program = lower(model, example)
-    return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine)
+    return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine,
+                          bound_grids)
 
 
 def static_dag(program: Program, gpu_config: GpuConfig | None = None,
-               conv_engine: str = "tc") -> ComputationGraph:
+               conv_engine: str = "tc", bound_grids: bool = False) -> ComputationGraph:
     """CPU-only DAG of a lowered program: demands from each op's launch
     configuration (no profiling; registers 0 and a unit block time unless a GPU
     is present).  Used by CPU tests and to produce reference fixtures."""
     cfg = gpu_config or GPU_PRESETS["b200"]
+    targets = concurrency_targets(program) if bound_grids else {}
     nodes = []
     dummy = []
     for k, op in enumerate(program.ops):
         views = ((0x1000, 0, op.inputs[0].root()[0].shape[-1], op.inputs[0].root()[0].nchw_input),
                  (0x2000, op.output.root()[1], op.output.root()[0].shape[-1]))
-        rec = _op_record(op, views, (0x3000, 0x4000), conv_engine_for(op, CONV_ENGINES[conv_engine]))
+        rec = _op_record(op, views, (0x3000, 0x4000), conv_engine_for(op, CONV_ENGINES[conv_engine]),
+                         targets.get(k, 0))
         prof = _lib.OparaOpProfile()
         _lib.check(_lib.lib().opara_op_launch_config(C.byref(rec), C.byref(prof)))
         d = ResourceDemand(prof.threads_per_block, prof.shared_mem_per_block,
