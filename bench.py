@@ -163,7 +163,7 @@ def run_gpu(args) -> dict | None:
     from paper_2312_10351_b200.dag import graph_to_dict
 
     model, x = zoo.build(args.model)
-    sg = engine.compile(model, x, device=local, bound_grids=args.bounded)
+    sg = engine.compile(model, x, device=local, bound_grids=args.bounded, profile_reps=args.profile_reps)
     xd = x.cuda(local)
     # correctness guard on every rank: a fast wrong answer is not a result
     y = sg.run(xd)
@@ -208,38 +208,69 @@ def run_gpu(args) -> dict | None:
     work = sg.work()
     cp_us = sg.critical_path_us()
     lat_ms = t_par.median_ms
-    # DAG roofline: max(critical path, FLOPs at compute peak + bytes at HBM peak)
-    flop_term_us = work["flops"] / (FP32_SIMT_NOMINAL_TFLOPS * 1e12) * 1e6
-    byte_term_us = work["bytes"] / (peaks["hbm_gbs"] * 1e9) * 1e6
-    roof_us = max(cp_us, flop_term_us + byte_term_us)
-
-    # dominant kernel family: share of summed isolated time
+    # Compute peaks per engine.  tcgen05 kind::tf32 runs at half the bf16 rate
+    # (tensor throughput scales with operand bytes), and 3xTF32 issues three
+    # MMAs per product: effective peak = measured bf16 / 2 / 3.  The SIMT
+    # engine's peak is the nominal fp32 FFMA rate (no measured figure exists).
+    tc_peak_tflops = peaks["bf16_tflops"] / 2 / 3
     fam = {}
     for op, p in zip(sg.program.ops, sg.profile):
         if op.kind == 0:
             continue
-        f = fam.setdefault(op.kind, {"us": 0.0, "flops": 0, "bytes": 0, "launches": 0})
+        if op.kind == 1:
+            name = "conv2d_tc_tf32x3" if engine.conv_engine_for(op, sg.conv_engine) == 1 else "conv2d_f32_simt"
+        else:
+            name = {2: "maxpool2d", 3: "avgpool2d", 4: "global_avgpool", 5: "linear_f32"}[op.kind]
+        f = fam.setdefault(name, {"us": 0.0, "flops": 0, "bytes": 0, "launches": 0})
         f["us"] += p["isolated_us"]
         f["flops"] += op.flops
         f["bytes"] += op.bytes_min
         f["launches"] += 1
-    kind_names = {1: "conv2d_f32_simt", 2: "maxpool2d", 3: "avgpool2d", 4: "global_avgpool", 5: "linear_f32"}
-    dom_kind = max(fam, key=lambda k: fam[k]["us"])
-    d = fam[dom_kind]
+    peak_of = {"conv2d_tc_tf32x3": tc_peak_tflops, "conv2d_f32_simt": FP32_SIMT_NOMINAL_TFLOPS,
+               "linear_f32": FP32_SIMT_NOMINAL_TFLOPS}
+    # DAG roofline: max(critical path, FLOPs at compute peak + bytes at HBM peak)
+    flop_term_us = sum(f["flops"] / (peak_of.get(k, FP32_SIMT_NOMINAL_TFLOPS) * 1e12) * 1e6
+                       for k, f in fam.items() if k in peak_of)
+    byte_term_us = work["bytes"] / (peaks["hbm_gbs"] * 1e9) * 1e6
+    roof_us = max(cp_us, flop_term_us + byte_term_us)
+
+    dom = max(fam, key=lambda k: fam[k]["us"])
+    d = fam[dom]
     total_us = sum(f["us"] for f in fam.values())
-    dom_tflops = d["flops"] / (d["us"] * 1e-6) / 1e12
+    if dom in peak_of:
+        achieved = d["flops"] / (d["us"] * 1e-6) / 1e12
+        peak, unit, bound = peak_of[dom], "TFLOP/s", "tensor"
+    else:
+        achieved = d["bytes"] / (d["us"] * 1e-6) / 1e9
+        peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
+    traffic = None
+    prof = ROOT / "profiles" / f"r01_{args.model}_full.md"
+    if prof.exists() and dom == "conv2d_tc_tf32x3":
+        vals = {}
+        for ln in prof.read_text().splitlines():
+            parts = [x.strip() for x in ln.split("|")]
+            if len(parts) > 3 and parts[1].startswith("dram__bytes_"):
+                mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(parts[2], 1)
+                vals[parts[1]] = float(parts[3]) * mult
+        if vals:
+            traffic = int(sum(vals.values()))
     roofline = {
-        "kernel": kind_names.get(dom_kind, str(dom_kind)),
-        "bound": "tensor" if dom_kind in (1, 5) else "hbm",
-        "achieved": round(dom_tflops, 3), "peak": round(FP32_SIMT_NOMINAL_TFLOPS, 1),
-        "unit": "TFLOP/s", "frac": round(dom_tflops / FP32_SIMT_NOMINAL_TFLOPS, 4),
-        "peak_source": "nominal fp32 FFMA (148 SM x 128 lanes x 2 x 1.965 GHz); "
-                       "MEASURED_PEAKS.json holds bf16/HBM only",
-        "traffic": None,
+        "kernel": dom,
+        "bound": bound,
+        "achieved": round(achieved, 3), "peak": round(peak, 1),
+        "unit": unit, "frac": round(achieved / peak, 4),
+        "peak_source": ("measured bf16 (MEASURED_PEAKS.json) / 2 (tf32 rate) / 3 (3xTF32 passes)"
+                        if dom == "conv2d_tc_tf32x3" else
+                        "nominal fp32 FFMA (148 SM x 128 lanes x 2 x 1.965 GHz)" if unit == "TFLOP/s"
+                        else "measured HBM copy (MEASURED_PEAKS.json)"),
+        "traffic": traffic,
+        "traffic_note": "dram read+write bytes of one launch from the committed ncu --set full capture "
+                        "(cold cache under ncu)" if traffic else None,
         "share_of_step": round(d["us"] / total_us, 3),
         "launches_per_step": d["launches"],
         "flops_per_step": d["flops"],
-        "timing": "per-op CUDA-event timing of a graph of back-to-back launches (opara_exec_profile)",
+        "timing": "CUDA events around a graph of back-to-back launches of each op (opara_exec_profile), "
+                  "summed over the family's launches",
     }
 
     # CPU baseline: the reference's path on the same profiled DAG, 1 core
@@ -283,7 +314,8 @@ def run_gpu(args) -> dict | None:
                          "byte_term_us": round(byte_term_us, 2), "roofline_us": round(roof_us, 2),
                          "frac": round(roof_us / (lat_ms * 1e3), 4),
                          "flops": work["flops"], "bytes": work["bytes"],
-                         "compute_peak": "fp32 FFMA nominal 74.4 TF/s", "hbm_peak_gbs": peaks["hbm_gbs"]},
+                         "compute_peak_tflops": {k: round(v, 1) for k, v in peak_of.items()},
+                         "hbm_peak_gbs": peaks["hbm_gbs"]},
         "roofline": roofline,
         "rel_err_vs_torch_fp32": rel,
         "e2e": {"value": round(world * args.steps / e2e_s, 2), "unit": "inferences/s",
@@ -358,6 +390,8 @@ def main(argv=None) -> int:
     ap.add_argument("--model", default="inception_v3", choices=["inception_v3", "googlenet"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--profile-reps", type=int, default=20,
+                    help="launches per op when measuring its isolated in-graph time")
     ap.add_argument("--bounded", action="store_true",
                     help="size each conv for its DAG level's share of the SMs (Opara bounded grids) "
                          "instead of the whole GPU")

@@ -147,5 +147,43 @@ def main() -> None:
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(cases)} cases)")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def model_dags() -> None:
+    """Model DAG fixtures: the GoogLeNet / Inception-v3 DAGs our frontend
+    extracts (static launch-config demands), scheduled by the REFERENCE."""
+    sys.path.insert(0, str(REF))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+    from opsched import GpuConfig, allocate_streams, make_order
+    from opsched.graph import load_graph
+    from paper_2312_10351_b200 import engine, frontend, zoo
+    from paper_2312_10351_b200.dag import graph_to_dict
+    import tempfile
+
+    cfg = GpuConfig(148, 2048, 233472, 65536, 32)
+    out = {}
+    for name in ("googlenet", "inception_v3"):
+        model, x = zoo.build(name)
+        g = engine.static_dag(frontend.lower(model, x))
+        d = graph_to_dict(g)
+        with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+            json.dump(d, f)
+        rg = load_graph(f.name)  # the reference parses our DAG file
+        plan = allocate_streams(rg)
+        out[name] = {
+            "graph": d,
+            "assignment": [[v, plan.assignment[v]] for v in sorted(plan.assignment)],
+            "num_streams": plan.num_streams,
+            "sync": [list(e) for e in plan.sync_events],
+            "opara": list(make_order(rg, "opara", cfg).order),
+            "sequential": list(make_order(rg, "sequential", cfg).order),
+        }
+    path = OUT.with_name("model_dags_golden.json")
+    path.write_text(json.dumps(out, separators=(",", ":")) + "\n")
+    print(f"wrote {path} ({path.stat().st_size} bytes)")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "models":
+    model_dags()

@@ -1,0 +1,116 @@
+"""CPU-side checks of the model path: fx lowering, concat elimination, the
+static DAG, and bit-exact scheduling of the model DAGs against what the
+reference computed on the same DAG JSON (tests/golden/model_dags_golden.json)."""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2312_10351_b200 as op
+from conftest import GOLDEN
+from oracle import opsched_oracle as orc
+from paper_2312_10351_b200 import engine, frontend, zoo
+from paper_2312_10351_b200.dag import graph_from_dict, graph_to_dict
+
+MODELS = json.loads((GOLDEN / "model_dags_golden.json").read_text())
+B200 = op.GPU_PRESETS["b200"]
+
+
+@pytest.mark.parametrize("name", sorted(MODELS))
+def test_model_dag_schedule_matches_reference(name):
+    gold = MODELS[name]
+    g = graph_from_dict(gold["graph"])
+    plan = op.allocate_streams(g)
+    assert sorted(plan.assignment.items()) == [tuple(x) for x in gold["assignment"]]
+    assert plan.num_streams == gold["num_streams"]
+    assert [list(e) for e in plan.sync_events] == gold["sync"]
+    assert list(op.order_opara(g, B200).order) == gold["opara"]
+    assert list(op.make_order(g, "sequential", B200).order) == gold["sequential"]
+
+
+@pytest.mark.parametrize("name,v,e,streams", [("googlenet", 81, 107, 28), ("inception_v3", 124, 158, 36)])
+def test_lowering_matches_fixture_and_paper_anchor(name, v, e, streams):
+    """Our frontend reproduces the committed DAG exactly; GoogLeNet's 28
+    streams equal the paper's count."""
+    model, x = zoo.build(name)
+    prog = frontend.lower(model, x)
+    g = engine.static_dag(prog)
+    d = graph_to_dict(g)
+    gold = MODELS[name]["graph"]
+    assert d["edges"] == gold["edges"]
+    assert [(n["id"], n["name"], n["class"]) for n in d["nodes"]] == \
+           [(n["id"], n["name"], n["class"]) for n in gold["nodes"]]
+    assert (len(g), len(g.edges), op.allocate_streams(g).num_streams) == (v, e, streams)
+
+
+def test_concat_slices_are_disjoint_and_cover():
+    model, x = zoo.build("googlenet")
+    prog = frontend.lower(model, x)
+    for k, o in enumerate(prog.ops):
+        if o.kind != frontend.NOP:
+            continue
+        root, base = o.output.root()
+        spans = sorted((t.root()[1], t.root()[1] + t.shape[3]) for t in o.inputs)
+        assert spans[0][0] == base and spans[-1][1] == base + o.output.shape[3]
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_bn_folding_is_exact_in_float64():
+    torch.manual_seed(0)
+    conv = torch.nn.Conv2d(8, 16, 3, padding=1, bias=False)
+    bn = torch.nn.BatchNorm2d(16, eps=1e-3)
+    with torch.no_grad():
+        bn.running_mean.normal_(0, 0.1)
+        bn.running_var.uniform_(0.5, 1.5)
+        bn.weight.uniform_(0.5, 1.5)
+        bn.bias.normal_(0, 0.1)
+    bn.eval()
+    wk, b = frontend._fold_bn(conv, bn)
+    x = torch.randn(1, 8, 5, 5)
+    ref = bn(conv(x)).detach()
+    w = torch.from_numpy(wk).reshape(3, 3, 8, 16).permute(3, 2, 0, 1)
+    y = torch.nn.functional.conv2d(x, w, torch.from_numpy(b), padding=1)
+    assert torch.allclose(y, ref, atol=1e-5)
+
+
+def test_static_dag_schedules_equal_oracle():
+    model, x = zoo.build("inception_v3")
+    g = engine.static_dag(frontend.lower(model, x))
+    d = graph_to_dict(g)
+    o = orc.Dag(d["nodes"], d["edges"])
+    a, ns, sync = orc.allocate_streams(o)
+    plan = op.allocate_streams(g)
+    assert dict(plan.assignment) == a and plan.num_streams == ns
+    cfg = {"threads_per_sm": B200.threads_per_sm, "shared_mem_per_sm": B200.shared_mem_per_sm,
+           "registers_per_sm": B200.registers_per_sm}
+    assert list(op.order_opara(g, B200).order) == orc.order_opara(o, cfg)
+
+
+def test_pack_conv_weights_layout():
+    """The tcgen05 W image: 64-byte swizzle, hi + lo == w (tf32 split)."""
+    rng = np.random.default_rng(0)
+    wk = rng.standard_normal((40, 130)).astype(np.float32)  # K=40, Cout=130
+    p = engine.pack_conv_weights_tf32x3(wk)
+    mt, kb = 2, 3
+    img = p.reshape(mt, kb, 2, 16, 8, 4, 4)
+    for co in (0, 7, 77, 129):
+        for k in (0, 5, 17, 39):
+            m, row = divmod(co, 128)
+            atom, r = divmod(row, 8)
+            b, kk = divmod(k, 16)
+            pos = (kk // 4) ^ ((r >> 1) & 3)
+            hi = img[m, b, 0, atom, r, pos, kk % 4]
+            lo = img[m, b, 1, atom, r, pos, kk % 4]
+            assert hi + lo == pytest.approx(float(wk[k, co]), rel=1e-6)
+            assert (np.float32(hi).view(np.uint32) & 0x1FFF) == 0
+
+
+def test_concurrency_targets_share_levels():
+    model, x = zoo.build("googlenet")
+    prog = frontend.lower(model, x)
+    t = engine.concurrency_targets(prog)
+    assert t and all(8 <= v <= 148 for v in t.values())

@@ -1,0 +1,49 @@
+"""N>1 plumbing on CPU: every rank builds its own replica schedule (no data
+collective), and the timing reduction is a max over ranks (gloo, world 2)."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    import paper_2312_10351_b200 as op
+    from paper_2312_10351_b200 import engine, frontend, zoo
+    model, x = zoo.build("googlenet")
+    g = engine.static_dag(frontend.lower(model, x))
+    plan = op.allocate_streams(g)
+    order = op.order_opara(g, op.GPU_PRESETS["b200"]).order
+    fake_seconds = torch.tensor([1.0 + rank], dtype=torch.float64)
+    dist.all_reduce(fake_seconds, op=dist.ReduceOp.MAX)
+    q.put((rank, plan.num_streams, hash(order), float(fake_seconds)))
+    dist.destroy_process_group()
+
+
+def test_two_replicas_schedule_identically_and_time_is_max():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0][1:3] == res[1][1:3] == (28, res[0][2])
+    assert res[0][3] == res[1][3] == 2.0
