@@ -163,7 +163,8 @@ def run_gpu(args) -> dict | None:
     from paper_2312_10351_b200.dag import graph_to_dict
 
     model, x = zoo.build(args.model)
-    sg = engine.compile(model, x, device=local, bound_grids=args.bounded, profile_reps=args.profile_reps)
+    sg = engine.compile(model, x, device=local, bound_grids=args.bounded, profile_reps=args.profile_reps,
+                        dtype=args.dtype)
     xd = x.cuda(local)
     # correctness guard on every rank: a fast wrong answer is not a result
     y = sg.run(xd)
@@ -296,9 +297,9 @@ def run_gpu(args) -> dict | None:
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32",
+        "dtype": args.dtype,
         "data": "synthetic input, random-init weights (seed 0), BN stats randomised",
-        "config": {"workload": f"{args.model} batch=1 fp32 ({'x'.join(map(str, x.shape))} NCHW)",
+        "config": {"workload": f"{args.model} batch=1 {args.dtype} ({'x'.join(map(str, x.shape))} NCHW)",
                    "parallelism": f"{world} independent replica(s), no collective",
                    "l2": "flushed (256 MiB memset) before every timed step, outside the event bracket",
                    "dag_nodes": len(sg.graph), "dag_edges": len(sg.graph.edges),
@@ -318,6 +319,7 @@ def run_gpu(args) -> dict | None:
                          "hbm_peak_gbs": peaks["hbm_gbs"]},
         "roofline": roofline,
         "rel_err_vs_torch_fp32": rel,
+        "rel_tolerance": 1e-4 if args.dtype == "f32" else 1e-2,
         "e2e": {"value": round(world * args.steps / e2e_s, 2), "unit": "inferences/s",
                 "h2d_bytes_per_step": e2e["h2d_bytes"], "d2h_bytes_per_step": e2e["d2h_bytes"],
                 "path": "ScheduledGraph.run_host: pinned host NCHW input -> H2D -> graph replay -> "
@@ -390,6 +392,7 @@ def main(argv=None) -> int:
     ap.add_argument("--model", default="inception_v3", choices=["inception_v3", "googlenet"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--profile-reps", type=int, default=20,
                     help="launches per op when measuring its isolated in-graph time")
     ap.add_argument("--bounded", action="store_true",

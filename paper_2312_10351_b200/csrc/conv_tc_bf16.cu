@@ -1,0 +1,480 @@
+// bf16 NHWC implicit-GEMM convolution / linear layer on tcgen05 (kind::f16,
+// bf16 operands, fp32 accumulation in TMEM).  Same GEMM view as the 3xTF32
+// engine (conv_tc.cu): weights on M (128 output channels per tile), output
+// pixels (or tokens, for a linear layer = 1x1 conv over a [tokens][K] map) on
+// N = BN, k = (r*S + s)*Cin + c.
+//
+// One pass, one operand plane each, so the ring is deeper and lighter:
+//   warps 0-3  gather: im2col with cp.async (16 B = 8 bf16 channels, zero-fill
+//              for padding) into 64-byte-swizzled K-major atoms; completion is
+//              signalled straight onto the stage's `full` mbarrier
+//              (cp.async.mbarrier.arrive.noinc).  Inputs that are not 8-channel
+//              aligned (stems, the fp32 NCHW graph input) take a register path
+//              that converts to bf16 and arrives after fence.proxy.async;
+//   warp 4     weight loader: one cp.async.bulk of the host-packed 8 KB W block;
+//   warp 5     MMA issuer: 2 x tcgen05.mma (K = 16) per 32-wide k step.
+// Epilogue as in conv_tc.cu: TMEM -> smem tile -> (cluster split-K DSMEM
+// reduction in rank order) -> + bias, activation (none/ReLU/GELU-erf), store
+// bf16 or fp32 into the output channel view.
+
+#include <cuda_bf16.h>
+
+#include <map>
+#include <mutex>
+#include <type_traits>
+
+#include "device_common.cuh"
+#include "ops.h"
+#include "status.h"
+#include "tc_common.cuh"
+
+namespace opara {
+namespace {
+
+constexpr int kBK = 32;                     // bf16 k elements per stage (64 B rows)
+constexpr int kGatherWarps = 4;
+constexpr int kLoadWarp = 4, kMmaWarp = 5;
+constexpr int kThreads = 192;
+constexpr int kMaxSplits = 8;
+constexpr uint32_t kWBytes = 128 * kBK * 2;  // 8 KB
+
+__host__ __device__ constexpr int bf_stages(int bn) { return bn <= 64 ? 8 : 6; }
+
+enum GatherMode { kVecBf16 = 0, kScalarBf16 = 1, kScalarF32 = 2 };
+
+struct BfArgs {
+  const void* in;
+  const __nv_bfloat16* __restrict__ wpack;  // [m_tiles][kblocks][atom][row][chunk][8]
+  const float* __restrict__ bias;
+  void* out;
+  int N, H, W, Cin, in_coff;
+  int OH, OW, Cout, out_cs, out_coff;
+  int R, S, sh, sw, ph, pw;
+  int act, vec_out;
+  int M, K, kblocks;
+  int splits, kb_per_split;
+  int64_t sN, sH, sW, sC;
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+
+__device__ __forceinline__ float act_fn(float v, int act) {
+  if (act == 1) return fmaxf(v, 0.f);
+  if (act == 2) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+  if (act == 3) return tanhf(v);
+  return v;
+}
+
+template <int BN, int kMode, typename TO>
+__global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned long long* trace) {
+  constexpr int kStages = bf_stages(BN);
+  constexpr uint32_t kXBytes = BN * kBK * 2;
+  constexpr uint32_t kStage = kWBytes + kXBytes;
+  constexpr uint32_t kSbo = 512;
+  constexpr int kRowGroups = BN / 8;
+  constexpr int kRowsPerThread = (kRowGroups + 3) / 4;
+  constexpr uint32_t kIdesc = tc::instr_desc(1, 128, BN);
+  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  static_assert(BN * 128 * 4 <= kStages * kStage, "epilogue tile must fit in the pipeline smem");
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
+  uint64_t* empty = full + kStages;
+  uint64_t* accum = empty + kStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  trace_begin(trace);
+  pdl_trigger();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n0 = blockIdx.x * BN;
+  const int mt = blockIdx.y;
+  const int kb0 = blockIdx.z * a.kb_per_split;
+  const int nkb = min(a.kblocks, kb0 + a.kb_per_split) - kb0;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full[s], 32 * kGatherWarps + 1);  // gather threads + the weight loader
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(accum, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, kTmemCols);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp < kGatherWarps) {
+    // ------------------------------------------------------------ gather
+    const int rw = warp, r8 = lane & 7, cl = lane >> 3;
+    auto x_off = [&](int j) -> uint32_t {
+      return static_cast<uint32_t>(rw + 4 * j) * kSbo + r8 * 64u +
+             static_cast<uint32_t>((cl ^ ((r8 >> 1) & 3)) * 16);
+    };
+    int pb[kRowsPerThread], pih[kRowsPerThread], piw[kRowsPerThread];
+    const int ohw = a.OH * a.OW;
+#pragma unroll
+    for (int j = 0; j < kRowsPerThread; ++j) {
+      const int p = n0 + (rw + 4 * j) * 8 + r8;
+      if (rw + 4 * j < kRowGroups && p < a.M) {
+        const int b = p / ohw, rem = p - b * ohw, oh = rem / a.OW, ow = rem - oh * a.OW;
+        pb[j] = b;
+        pih[j] = oh * a.sh - a.ph;
+        piw[j] = ow * a.sw - a.pw;
+      } else {
+        pb[j] = -1;
+        pih[j] = 0;
+        piw[j] = 0;
+      }
+    }
+    pdl_wait();
+    if constexpr (kMode == kVecBf16) {
+      const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(a.in);
+      const __nv_bfloat16* rowbase[kRowsPerThread];
+#pragma unroll
+      for (int j = 0; j < kRowsPerThread; ++j)
+        rowbase[j] = in + (pb[j] >= 0 ? pb[j] * a.sN + pih[j] * a.sH + piw[j] * a.sW + a.in_coff : 0);
+      int kc = kb0 * kBK + cl * 8, dc = 0, dr = 0, dq = 0;
+      if (kc < a.K) {
+        dc = kc % a.Cin;
+        const int rs = kc / a.Cin;
+        dr = rs / a.S;
+        dq = rs - dr * a.S;
+      }
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        const uint32_t xs = tc::smem_u32(smem + s * kStage + kWBytes);
+        const bool kin = kc < a.K;
+        const int64_t koff = dr * a.sH + dq * a.sW + dc;
+#pragma unroll
+        for (int j = 0; j < kRowsPerThread; ++j) {
+          const int ih = pih[j] + dr, iw = piw[j] + dq;
+          const bool ok = kin && pb[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+          if (rw + 4 * j < kRowGroups) cp_async16(xs + x_off(j), ok ? rowbase[j] + koff : in, ok);
+        }
+        tc::cp_async_arrive_noinc(&full[s]);
+        kc += kBK;
+        dc += kBK;
+        while (dc >= a.Cin) {
+          dc -= a.Cin;
+          if (++dq == a.S) {
+            dq = 0;
+            ++dr;
+          }
+        }
+      }
+    } else {
+      using TIn = typename std::conditional<kMode == kScalarF32, float, __nv_bfloat16>::type;
+      const TIn* in = static_cast<const TIn*>(a.in);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        uint8_t* xs = smem + s * kStage + kWBytes;
+        const int kbase = (kb0 + i) * kBK + cl * 8;
+        __nv_bfloat16 v[kRowsPerThread][8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int k = kbase + e;
+          const bool kin = k < a.K;
+          int c = 0, r = 0, q = 0;
+          if (kin) {
+            c = k % a.Cin;
+            const int rs = k / a.Cin;
+            r = rs / a.S;
+            q = rs - r * a.S;
+          }
+#pragma unroll
+          for (int j = 0; j < kRowsPerThread; ++j) {
+            const int ih = pih[j] + r, iw = piw[j] + q;
+            const bool ok = kin && pb[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+            float x = 0.f;
+            if (ok) {
+              const TIn t = in[pb[j] * a.sN + ih * a.sH + iw * a.sW + c * a.sC + a.in_coff];
+              if constexpr (kMode == kScalarF32) x = t; else x = __bfloat162float(t);
+            }
+            v[j][e] = __float2bfloat16_rn(x);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kRowsPerThread; ++j)
+          if (rw + 4 * j < kRowGroups) *reinterpret_cast<uint4*>(xs + x_off(j)) = *reinterpret_cast<const uint4*>(v[j]);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&full[s]);
+      }
+    }
+  } else if (warp == kLoadWarp) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&full[s], kWBytes);
+        const __nv_bfloat16* src = a.wpack + (static_cast<int64_t>(mt) * a.kblocks + kb0 + i) * (kWBytes / 2);
+        tc::bulk_g2s(smem + s * kStage, src, kWBytes, &full[s]);
+      }
+    }
+  } else if (lane == 0) {
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kStages;
+      tc::mbar_wait(&full[s], (i / kStages) & 1);
+      tc::tc_fence_after();
+      const uint32_t base = tc::smem_u32(smem + s * kStage);
+#pragma unroll
+      for (int ks = 0; ks < kBK / 16; ++ks) {
+        const uint64_t ad = tc::smem_desc_sw64(base + 32 * ks, kSbo);
+        const uint64_t bd = tc::smem_desc_sw64(base + kWBytes + 32 * ks, kSbo);
+        tc::mma_f16(tmem, ad, bd, kIdesc, (i | ks) != 0);
+      }
+      tc::mma_commit(&empty[s]);
+    }
+    tc::mma_commit(accum);
+  }
+  __syncwarp();
+
+  // ------------------------------------------------------------ epilogue
+  float* tile = reinterpret_cast<float*>(smem);
+  if (warp < 4) {
+    tc::mbar_wait(accum, 0);
+    tc::tc_fence_after();
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 4
+    for (int c8 = 0; c8 < BN / 8; ++c8) {
+      float v[8];
+      tc::tmem_ld8(trow + c8 * 8, v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) tile[(c8 * 8 + e) * 128 + warp * 32 + lane] = v[e];
+    }
+  }
+  tc::tc_fence_before();
+  const int splits = a.splits;
+  if (splits > 1)
+    tc::cluster_sync();
+  else
+    __syncthreads();
+  const int rank = splits > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
+  const int rows_per = (BN + splits - 1) / splits;
+  const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
+  const int ch = mt * 128 + lane * 4;
+  float bias[4] = {0.f, 0.f, 0.f, 0.f};
+  if (a.bias) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (ch + e < a.Cout) bias[e] = __ldg(a.bias + ch + e);
+  }
+  const uint32_t tile_s = tc::smem_u32(tile);
+  TO* out = static_cast<TO*>(a.out);
+  for (int row = r0 + warp; row < r1; row += kThreads / 32) {
+    const int p = n0 + row;
+    if (p >= a.M) break;
+    const uint32_t off = static_cast<uint32_t>((row * 128 + lane * 4) * 4);
+    float4 acc;
+    if (splits > 1) {
+      float4 part[kMaxSplits];
+#pragma unroll
+      for (int z = 0; z < kMaxSplits; ++z)
+        if (z < splits) part[z] = tc::ld_dsmem_f4(tc::map_cluster(tile_s + off, z));
+      acc = part[0];
+#pragma unroll
+      for (int z = 1; z < kMaxSplits; ++z)
+        if (z < splits) {
+          acc.x += part[z].x; acc.y += part[z].y; acc.z += part[z].z; acc.w += part[z].w;
+        }
+    } else {
+      acc = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(tile) + off);
+    }
+    float y[4] = {act_fn(acc.x + bias[0], a.act), act_fn(acc.y + bias[1], a.act),
+                  act_fn(acc.z + bias[2], a.act), act_fn(acc.w + bias[3], a.act)};
+    TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
+    if constexpr (std::is_same<TO, float>::value) {
+      if (a.vec_out && ch + 3 < a.Cout) {
+        *reinterpret_cast<float4*>(dst) = make_float4(y[0], y[1], y[2], y[3]);
+        continue;
+      }
+    } else {
+      if (a.vec_out && ch + 3 < a.Cout) {
+        __nv_bfloat162 lo2 = __floats2bfloat162_rn(y[0], y[1]);
+        __nv_bfloat162 hi2 = __floats2bfloat162_rn(y[2], y[3]);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo2);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi2);
+        *reinterpret_cast<uint2*>(dst) = pk;
+        continue;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (ch + e < a.Cout) {
+        if constexpr (std::is_same<TO, float>::value) dst[e] = y[e];
+        else dst[e] = __float2bfloat16_rn(y[e]);
+      }
+    }
+  }
+  if (splits > 1) tc::cluster_sync();
+  else __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, kTmemCols);
+  }
+  trace_end(trace);
+}
+
+template <int BN>
+constexpr size_t bf_smem_bytes() {
+  return bf_stages(BN) * (kWBytes + static_cast<size_t>(BN) * kBK * 2) + 256 + 1024;
+}
+
+struct BfVariant {
+  int bn;
+  const void* func[3][2];  // [gather mode][out bf16, out f32]
+  size_t smem;
+};
+
+template <int BN>
+BfVariant make_bf() {
+  BfVariant v;
+  v.bn = BN;
+  v.func[kVecBf16][0] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kVecBf16, __nv_bfloat16>);
+  v.func[kVecBf16][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kVecBf16, float>);
+  v.func[kScalarBf16][0] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kScalarBf16, __nv_bfloat16>);
+  v.func[kScalarBf16][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kScalarBf16, float>);
+  v.func[kScalarF32][0] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kScalarF32, __nv_bfloat16>);
+  v.func[kScalarF32][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kScalarF32, float>);
+  v.smem = bf_smem_bytes<BN>();
+  return v;
+}
+
+const BfVariant* bf_variants() {
+  static const BfVariant v[] = {make_bf<32>(), make_bf<64>(), make_bf<128>(), make_bf<256>()};
+  return v;
+}
+
+opara_status set_attr_once(const void* func, size_t smem) {
+  static std::mutex mu;
+  static std::map<const void*, bool> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[func]) return OPARA_OK;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return cuda_fail(e, "conv2d_tc_bf16 smem attribute");
+  done[func] = true;
+  return OPARA_OK;
+}
+
+int64_t max_clusters(const void* func, int size, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int64_t> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(func, size);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int64_t result = 2 * 148 / size;
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0 &&
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) == cudaSuccess) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(1, 1, size);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = size;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, func, &lc) == cudaSuccess && n > 0) result = n;
+  }
+  cudaGetLastError();
+  cache[key] = result;
+  return result;
+}
+
+}  // namespace
+
+// CONV2D with i[22] == 2 (engine "tc_bf16"): i[18] = input dtype (0 f32, 1 bf16),
+// i[23] = output dtype, i[24] = activation (0 none, 1 ReLU, 2 GELU; i[17]
+// relu=1 also selects ReLU); p[1] = bf16 weights packed by
+// engine.pack_conv_weights_bf16.
+opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned long long* trace,
+                                   LaunchCfg* cfg, bool dry) {
+  BfArgs a;
+  a.in = op.p[0];
+  a.wpack = static_cast<const __nv_bfloat16*>(op.p[1]);
+  a.bias = static_cast<const float*>(op.p[2]);
+  a.out = op.p[3];
+  a.N = (int)op.i[0]; a.H = (int)op.i[1]; a.W = (int)op.i[2]; a.Cin = (int)op.i[3];
+  const int in_cs = (int)op.i[4];
+  a.in_coff = (int)op.i[5];
+  a.OH = (int)op.i[6]; a.OW = (int)op.i[7]; a.Cout = (int)op.i[8];
+  a.out_cs = (int)op.i[9]; a.out_coff = (int)op.i[10];
+  a.R = (int)op.i[11]; a.S = (int)op.i[12]; a.sh = (int)op.i[13]; a.sw = (int)op.i[14];
+  a.ph = (int)op.i[15]; a.pw = (int)op.i[16];
+  a.act = op.i[24] ? (int)op.i[24] : (op.i[17] ? 1 : 0);
+  const bool in_f32 = op.i[18] == 0;
+  const bool out_f32 = op.i[23] == 0;
+  a.M = a.N * a.OH * a.OW;
+  a.K = a.R * a.S * a.Cin;
+  a.kblocks = (a.K + kBK - 1) / kBK;
+  const bool nchw = op.i[20] != 0;
+  if (nchw) {
+    a.sC = static_cast<int64_t>(a.H) * a.W;
+    a.sW = 1;
+    a.sH = a.W;
+    a.sN = a.sC * a.Cin;
+    a.in_coff = 0;
+  } else {
+    a.sC = 1;
+    a.sW = in_cs;
+    a.sH = static_cast<int64_t>(a.W) * in_cs;
+    a.sN = a.sH * a.H;
+  }
+  if (a.M <= 0 || a.Cout <= 0 || a.K <= 0) return fail(OPARA_ERR_VALUE, "conv2d: empty shape");
+  const int mode = in_f32 ? kScalarF32
+                 : (!nchw && a.Cin % 8 == 0 && in_cs % 8 == 0 && a.in_coff % 8 == 0 &&
+                    reinterpret_cast<uintptr_t>(a.in) % 16 == 0) ? kVecBf16 : kScalarBf16;
+  const int align = out_f32 ? 16 : 8;
+  a.vec_out = (a.out_cs % 4 == 0 && a.out_coff % 4 == 0 && reinterpret_cast<uintptr_t>(a.out) % align == 0) ? 1 : 0;
+  const BfVariant* v = bf_variants();
+  const int mtiles = (a.Cout + 127) / 128;
+  int id = op.variant;
+  if (id < 0 || id > 3) {
+    id = 0;
+    const int bns[4] = {32, 64, 128, 256};
+    for (int k = 3; k >= 0; --k) {
+      const int64_t tiles = static_cast<int64_t>((a.M + bns[k] - 1) / bns[k]) * mtiles;
+      if (tiles >= 32 || k == 0) {
+        id = k;
+        break;
+      }
+    }
+  }
+  const int bn = v[id].bn;
+  const int64_t base = static_cast<int64_t>((a.M + bn - 1) / bn) * mtiles;
+  const int64_t target = op.i[21] > 0 ? op.i[21] : 148;
+  int64_t splits = op.i[19] > 1 ? op.i[19] : std::max<int64_t>(1, target / base);
+  splits = std::min<int64_t>(splits, kMaxSplits);
+  splits = std::min<int64_t>(splits, std::max(1, a.kblocks / 2));
+  splits = std::max<int64_t>(1, splits);
+  const void* func = v[id].func[mode][out_f32 ? 1 : 0];
+  if (splits > 1 && op.i[19] <= 1)
+    while (splits > 1 && base > max_clusters(func, static_cast<int>(splits), v[id].smem)) --splits;
+  a.kb_per_split = static_cast<int>((a.kblocks + splits - 1) / splits);
+  a.splits = (a.kblocks + a.kb_per_split - 1) / a.kb_per_split;
+  LaunchCfg c;
+  c.func = func;
+  c.grid = dim3(ceil_div(a.M, bn), mtiles, a.splits);
+  c.block = dim3(kThreads);
+  c.smem = v[id].smem;
+  if (cfg) *cfg = c;
+  if (dry) return OPARA_OK;
+  opara_status st = set_attr_once(func, c.smem);
+  if (st != OPARA_OK) return st;
+  void* args[] = {&a, &trace};
+  return launch_kernel(c, args, s, a.splits > 1 ? static_cast<unsigned>(a.splits) : 1u);
+}
+
+}  // namespace opara

@@ -69,7 +69,9 @@ opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* t
       if (cfg) *cfg = LaunchCfg{};
       return OPARA_OK;
     case OPARA_OP_CONV2D:
-      return op.i[22] == 1 ? launch_conv2d_tc(op, s, trace, cfg, dry) : launch_conv2d(op, s, trace, cfg, dry);
+      return op.i[22] == 2   ? launch_conv2d_tc_bf16(op, s, trace, cfg, dry)
+             : op.i[22] == 1 ? launch_conv2d_tc(op, s, trace, cfg, dry)
+                             : launch_conv2d(op, s, trace, cfg, dry);
     case OPARA_OP_MAXPOOL2D:
     case OPARA_OP_AVGPOOL2D: return launch_pool2d(op, s, trace, cfg, dry);
     case OPARA_OP_GLOBAL_AVGPOOL: return launch_global_avgpool(op, s, trace, cfg, dry);

@@ -58,6 +58,7 @@ using Launcher = opara_status (*)(const opara_op& op, cudaStream_t s, unsigned l
 
 opara_status launch_conv2d(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
 opara_status launch_conv2d_tc(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+opara_status launch_conv2d_tc_bf16(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
 opara_status launch_pool2d(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
 opara_status launch_global_avgpool(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*,
                                    bool);

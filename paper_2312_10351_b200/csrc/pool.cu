@@ -2,6 +2,8 @@
 // channels): 128-bit loads/stores when the channel view is 16-byte aligned,
 // scalar otherwise.  Grid-stride loops with a bounded grid.
 
+#include <cuda_bf16.h>
+
 #include "device_common.cuh"
 #include "ops.h"
 #include "status.h"
@@ -10,8 +12,8 @@ namespace opara {
 namespace {
 
 struct PoolArgs {
-  const float* __restrict__ in;
-  float* __restrict__ out;
+  const void* in;
+  void* out;
   int N, H, W, C, in_cs, in_coff;
   int OH, OW, out_cs, out_coff;
   int kh, kw, sh, sw, ph, pw;
@@ -20,8 +22,21 @@ struct PoolArgs {
 
 // Window semantics follow torch's pooling (max: padding never wins; avg:
 // divisor counts padded cells when count_include_pad, clipped at H+pad).
-template <bool kMax, int V>
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
+// V-wide vector of T (V = 4: 16 B for fp32, 8 B for bf16)
+template <typename T, int V> struct Vec;
+template <> struct Vec<float, 4> { using type = float4; };
+template <> struct Vec<__nv_bfloat16, 4> { using type = uint2; };
+
+template <bool kMax, int V, typename T>
 __global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long long* trace) {
+  const T* in = static_cast<const T*>(a.in);
+  T* outp = static_cast<T*>(a.out);
   trace_begin(trace);
   pdl_trigger();
   pdl_wait();
@@ -46,14 +61,16 @@ __global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long lon
     for (int v = 0; v < V; ++v) acc[v] = kMax ? -INFINITY : 0.f;
     for (int ih = hs; ih < he; ++ih) {
       for (int iw = ws; iw < we; ++iw) {
-        const float* src = a.in + (static_cast<int64_t>(b * a.H + ih) * a.W + iw) * a.in_cs + a.in_coff + c;
+        const T* src = in + (static_cast<int64_t>(b * a.H + ih) * a.W + iw) * a.in_cs + a.in_coff + c;
         float x[V];
         if constexpr (V == 4) {
-          const float4 t = __ldg(reinterpret_cast<const float4*>(src));
-          x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+          const typename Vec<T, 4>::type t = *reinterpret_cast<const typename Vec<T, 4>::type*>(src);
+          const T* e = reinterpret_cast<const T*>(&t);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) x[v] = to_f(e[v]);
         } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = __ldg(src + v);
+          for (int v = 0; v < V; ++v) x[v] = to_f(src[v]);
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -71,12 +88,16 @@ __global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long lon
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[v] = acc[v] / static_cast<float>(div);
     }
-    float* dst = a.out + q * a.out_cs + a.out_coff + c;
+    T* dst = outp + q * a.out_cs + a.out_coff + c;
     if constexpr (V == 4) {
-      *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      typename Vec<T, 4>::type t;
+      T* e = reinterpret_cast<T*>(&t);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) e[v] = from_f<T>(acc[v]);
+      *reinterpret_cast<typename Vec<T, 4>::type*>(dst) = t;
     } else {
 #pragma unroll
-      for (int v = 0; v < V; ++v) dst[v] = acc[v];
+      for (int v = 0; v < V; ++v) dst[v] = from_f<T>(acc[v]);
     }
   }
   trace_end(trace);
@@ -84,7 +105,8 @@ __global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long lon
 
 // Global average pool: one warp per (batch, 4-channel group) when C is large;
 // the warp strides over the H*W pixels and shuffles the partial sums.
-__global__ void __launch_bounds__(256) global_avgpool_nhwc(const float* __restrict__ in,
+template <typename T>
+__global__ void __launch_bounds__(256) global_avgpool_nhwc(const T* __restrict__ in,
                                                            float* __restrict__ out, int N, int HW,
                                                            int C, int in_cs, int in_coff,
                                                            unsigned long long* trace) {
@@ -100,7 +122,7 @@ __global__ void __launch_bounds__(256) global_avgpool_nhwc(const float* __restri
     const int b = static_cast<int>(w / C);
     float s = 0.f;
     for (int p = lane; p < HW; p += 32)
-      s += __ldg(in + (static_cast<int64_t>(b) * HW + p) * in_cs + in_coff + c);
+      s += to_f(in[(static_cast<int64_t>(b) * HW + p) * in_cs + in_coff + c]);
     s = warp_sum(s);
     if (lane == 0) out[static_cast<int64_t>(b) * C + c] = s / static_cast<float>(HW);
   }
@@ -109,7 +131,8 @@ __global__ void __launch_bounds__(256) global_avgpool_nhwc(const float* __restri
 
 // Small-HW variant: one thread per channel, sequential over pixels; coalesced
 // across channels (the common 7x7 / 8x8 tail of CNNs).
-__global__ void __launch_bounds__(128) global_avgpool_nhwc_cols(const float* __restrict__ in,
+template <typename T>
+__global__ void __launch_bounds__(128) global_avgpool_nhwc_cols(const T* __restrict__ in,
                                                                 float* __restrict__ out, int N,
                                                                 int HW, int C, int in_cs,
                                                                 int in_coff,
@@ -122,9 +145,9 @@ __global__ void __launch_bounds__(128) global_avgpool_nhwc_cols(const float* __r
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int c = static_cast<int>(t % C);
     const int b = static_cast<int>(t / C);
-    const float* src = in + static_cast<int64_t>(b) * HW * in_cs + in_coff + c;
+    const T* src = in + static_cast<int64_t>(b) * HW * in_cs + in_coff + c;
     float s = 0.f;
-    for (int p = 0; p < HW; ++p) s += __ldg(src + static_cast<int64_t>(p) * in_cs);
+    for (int p = 0; p < HW; ++p) s += to_f(src[static_cast<int64_t>(p) * in_cs]);
     out[t] = s / static_cast<float>(HW);
   }
   trace_end(trace);
@@ -135,28 +158,32 @@ __global__ void __launch_bounds__(128) global_avgpool_nhwc_cols(const float* __r
 opara_status launch_pool2d(const opara_op& op, cudaStream_t s, unsigned long long* trace,
                            LaunchCfg* cfg, bool dry) {
   PoolArgs a;
-  a.in = static_cast<const float*>(op.p[0]);
-  a.out = static_cast<float*>(op.p[3]);
+  a.in = op.p[0];
+  a.out = op.p[3];
   a.N = (int)op.i[0]; a.H = (int)op.i[1]; a.W = (int)op.i[2]; a.C = (int)op.i[3];
   a.in_cs = (int)op.i[4]; a.in_coff = (int)op.i[5];
   a.OH = (int)op.i[6]; a.OW = (int)op.i[7]; a.out_cs = (int)op.i[8]; a.out_coff = (int)op.i[9];
   a.kh = (int)op.i[10]; a.kw = (int)op.i[11]; a.sh = (int)op.i[12]; a.sw = (int)op.i[13];
   a.ph = (int)op.i[14]; a.pw = (int)op.i[15]; a.include_pad = (int)op.i[16];
-  if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "pool2d: fp32 only");
+  const bool bf = op.i[18] == 1;
   const bool is_max = op.kind == OPARA_OP_MAXPOOL2D;
   const bool vec = (a.C % 4 == 0) && (a.in_cs % 4 == 0) && (a.in_coff % 4 == 0) &&
                    (a.out_cs % 4 == 0) && (a.out_coff % 4 == 0) &&
-                   (reinterpret_cast<uintptr_t>(a.in) % 16 == 0) &&
-                   (reinterpret_cast<uintptr_t>(a.out) % 16 == 0);
+                   (reinterpret_cast<uintptr_t>(a.in) % (bf ? 8 : 16) == 0) &&
+                   (reinterpret_cast<uintptr_t>(a.out) % (bf ? 8 : 16) == 0);
   const int V = vec ? 4 : 1;
   const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
   LaunchCfg c;
-  if (is_max)
-    c.func = vec ? reinterpret_cast<const void*>(&pool2d_nhwc<true, 4>)
-                 : reinterpret_cast<const void*>(&pool2d_nhwc<true, 1>);
-  else
-    c.func = vec ? reinterpret_cast<const void*>(&pool2d_nhwc<false, 4>)
-                 : reinterpret_cast<const void*>(&pool2d_nhwc<false, 1>);
+  static const void* table[2][2][2] = {
+      {{reinterpret_cast<const void*>(&pool2d_nhwc<false, 1, float>),
+        reinterpret_cast<const void*>(&pool2d_nhwc<false, 4, float>)},
+       {reinterpret_cast<const void*>(&pool2d_nhwc<true, 1, float>),
+        reinterpret_cast<const void*>(&pool2d_nhwc<true, 4, float>)}},
+      {{reinterpret_cast<const void*>(&pool2d_nhwc<false, 1, __nv_bfloat16>),
+        reinterpret_cast<const void*>(&pool2d_nhwc<false, 4, __nv_bfloat16>)},
+       {reinterpret_cast<const void*>(&pool2d_nhwc<true, 1, __nv_bfloat16>),
+        reinterpret_cast<const void*>(&pool2d_nhwc<true, 4, __nv_bfloat16>)}}};
+  c.func = table[bf ? 1 : 0][is_max ? 1 : 0][vec ? 1 : 0];
   c.block = dim3(256);
   c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(work, 256), 148u * 4u)));
   if (cfg) *cfg = c;
@@ -167,20 +194,22 @@ opara_status launch_pool2d(const opara_op& op, cudaStream_t s, unsigned long lon
 
 opara_status launch_global_avgpool(const opara_op& op, cudaStream_t s, unsigned long long* trace,
                                    LaunchCfg* cfg, bool dry) {
-  const float* in = static_cast<const float*>(op.p[0]);
-  float* out = static_cast<float*>(op.p[3]);
+  const void* in = op.p[0];
+  float* out = static_cast<float*>(op.p[3]);  // always fp32 (feeds the classifier)
   int N = (int)op.i[0], H = (int)op.i[1], W = (int)op.i[2], C = (int)op.i[3];
   int in_cs = (int)op.i[4], in_coff = (int)op.i[5];
-  if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "global_avgpool: fp32 only");
+  const bool bf = op.i[18] == 1;
   int HW = H * W;
   LaunchCfg c;
   const int64_t total = static_cast<int64_t>(N) * C;
   if (HW <= 128) {
-    c.func = reinterpret_cast<const void*>(&global_avgpool_nhwc_cols);
+    c.func = bf ? reinterpret_cast<const void*>(&global_avgpool_nhwc_cols<__nv_bfloat16>)
+                : reinterpret_cast<const void*>(&global_avgpool_nhwc_cols<float>);
     c.block = dim3(128);
     c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(total, 128), 148u * 4u)));
   } else {
-    c.func = reinterpret_cast<const void*>(&global_avgpool_nhwc);
+    c.func = bf ? reinterpret_cast<const void*>(&global_avgpool_nhwc<__nv_bfloat16>)
+                : reinterpret_cast<const void*>(&global_avgpool_nhwc<float>);
     c.block = dim3(256);
     c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(total, 8), 148u * 4u)));
   }

@@ -57,19 +57,45 @@ def block_duration_us(isolated_us: float, d: ResourceDemand, cfg: GpuConfig) -> 
     return max(isolated_us / waves, 0.001)
 
 
-CONV_ENGINES = {"simt": 0, "tc": 1}
+CONV_ENGINES = {"simt": 0, "tc": 1, "tc_bf16": 2}
+DTYPE_CODE = {"f32": 0, "bf16": 1}
 
 
 def conv_engine_for(op, requested: int) -> int:
-    """Per-conv engine: the tensor-core kernel gathers 16-byte chunks of 4
-    channels, so convs over the raw NCHW graph input or with Cin % 4 != 0 (the
-    3-channel stems) run on the exact-fp32 SIMT kernel."""
-    if op.kind != CONV2D or requested != 1:
+    """Per-conv engine.  bf16 activations always use the bf16 tcgen05 kernel
+    (its register gather path also reads the fp32 NCHW graph input).  The
+    fp32 tensor-core kernel gathers 16-byte chunks of 4 channels, so fp32 convs
+    over the raw NCHW input or with Cin % 4 != 0 (the 3-channel stems) run on
+    the exact-fp32 SIMT kernel."""
+    if op.kind != CONV2D:
+        return requested
+    if op.output.dtype == "bf16":
+        return 2
+    if requested != 1:
         return requested
     x = op.inputs[0].root()[0]
     if x.nchw_input or op.ints["Cin"] % 4 != 0:
         return 0
     return 1
+
+
+def pack_conv_weights_bf16(wk: np.ndarray) -> np.ndarray:
+    """[K][Cout] conv weights -> bf16 UMMA images for conv_tc_bf16.cu: rows =
+    output channels (128-row tiles), 32-element k blocks, each (m-tile,
+    k-block) one contiguous 8 KiB record in 64-byte-swizzled K-major order
+    [atom(16)][row(8)][chunk(4), XOR (row >> 1) & 3][8 bf16].  Returned as
+    uint16 bit patterns (round to nearest even)."""
+    k, cout = wk.shape
+    mt, kb = -(-cout // 128), -(-k // 32)
+    w = np.zeros((mt * 128, kb * 32), dtype=np.float32)
+    w[:cout, :k] = wk.T
+    bits = torch.from_numpy(w).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    r = np.arange(8)[:, None]
+    c = np.arange(4)[None, :]
+    inv = np.argsort(c ^ ((r >> 1) & 3), axis=1)
+    t = bits.reshape(mt, 16, 8, kb, 4, 8).transpose(0, 3, 1, 2, 4, 5)  # (mt, kb, atom, r, chunk, e)
+    t = np.take_along_axis(t, inv[None, None, None, :, :, None], axis=4)
+    return np.ascontiguousarray(t).reshape(-1)
 
 
 def tf32_rna(x: np.ndarray) -> np.ndarray:
@@ -142,16 +168,19 @@ def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -
     (ib, icoff, ics, inchw), (ob, ocoff, ocs) = views
     i = rec.i
     if op.kind == CONV2D:
+        in_dt = DTYPE_CODE[op.inputs[0].root()[0].dtype]
         vals = [q["N"], q["H"], q["W"], q["Cin"], ics, icoff, q["OH"], q["OW"], q["Cout"], ocs, ocoff,
-                q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], 0, 1, int(inchw),
-                int(target_ctas), conv_engine]
+                q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], in_dt if conv_engine == 2 else 0,
+                1, int(inchw), int(target_ctas), conv_engine, DTYPE_CODE[op.output.dtype],
+                q.get("act", 1 if q["relu"] else 0)]
         rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
     elif op.kind in (MAXPOOL2D, AVGPOOL2D):
         vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff, q["OH"], q["OW"], ocs, ocoff, q["kh"],
-                q["kw"], q["sh"], q["sw"], q["ph"], q["pw"], q["include_pad"], 0, 0]
+                q["kw"], q["sh"], q["sw"], q["ph"], q["pw"], q["include_pad"], 0,
+                DTYPE_CODE[op.inputs[0].root()[0].dtype]]
         rec.p[0], rec.p[3] = ib, ob
     elif op.kind == GLOBAL_AVGPOOL:
-        vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff] + [0] * 12 + [0]
+        vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff] + [0] * 12 + [DTYPE_CODE[op.inputs[0].root()[0].dtype]]
         rec.p[0], rec.p[3] = ib, ob
     elif op.kind == LINEAR:
         vals = [q["M"], q["K"], q["N"], q["act"], q["K"], q["N"]] + [0] * 12 + [0]
@@ -219,11 +248,12 @@ class ScheduledGraph:
         for t in program.tensors:
             if t.alias is not None:
                 continue
+            tdt = torch.bfloat16 if t.dtype == "bf16" else torch.float32
             if t.nchw_input:
                 n, h, w, c = t.shape
-                buf = torch.zeros((n, c, h, w), dtype=torch.float32, device=self.dev)
+                buf = torch.zeros((n, c, h, w), dtype=tdt, device=self.dev)
             else:
-                buf = torch.zeros(t.shape, dtype=torch.float32, device=self.dev)
+                buf = torch.zeros(t.shape, dtype=tdt, device=self.dev)
             self._bufs[t.tid] = buf
         root, _ = program.input.root()
         self.input_buffer = self._bufs[root.tid]
@@ -244,8 +274,11 @@ class ScheduledGraph:
     def _weights(self, op):
         ptrs = []
         weight = op.weight
-        if op.kind == CONV2D and conv_engine_for(op, self.conv_engine) == 1:
+        eng = conv_engine_for(op, self.conv_engine) if op.kind == CONV2D else None
+        if eng == 1:
             weight = pack_conv_weights_tf32x3(op.weight)
+        elif eng == 2:
+            weight = pack_conv_weights_bf16(op.weight)
         for arr in (weight, op.bias):
             if arr is None:
                 ptrs.append(None)
@@ -356,8 +389,11 @@ class ScheduledGraph:
         s = torch.cuda.current_stream(self.dev)
         _lib.check(_lib.lib().opara_exec_trace(self._h, slot, C.c_void_p(s.cuda_stream),
                                                _lib.ptr(st), _lib.ptr(en)))
-        t0 = int(st.min())
-        return [(k + 1, int(st[k]) - t0, int(en[k]) - t0) for k in range(n)]
+        kern = [k for k in range(n) if self.program.ops[k].kind != NOP]
+        t0 = int(min(st[k] for k in kern)) if kern else 0
+        # NOP joins launch nothing: report them as zero-length at t = 0
+        return [(k + 1, int(st[k]) - t0, int(en[k]) - t0) if self.program.ops[k].kind != NOP else (k + 1, 0, 0)
+                for k in range(n)]
 
     def num_launches(self, slot: int = SLOT_PARALLEL) -> int:
         return int(_lib.lib().opara_exec_num_launches(self._h, slot))
@@ -400,12 +436,13 @@ class ScheduledGraph:
 
 
 def compile(model: torch.nn.Module, example: torch.Tensor, *, device: int = 0, policy: str = "opara",
+            dtype: str = "f32",
             gpu_config: GpuConfig | None = None, profile_reps: int = 20,
             seed: int | None = None, conv_engine: str = "tc",
             bound_grids: bool = False) -> ScheduledGraph:
     """Model in, scheduled graph out."""
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-    program = lower(model, example)
+    program = lower(model, example, dtype)
     return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine,
                           bound_grids)
 

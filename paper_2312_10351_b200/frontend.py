@@ -41,6 +41,7 @@ class Tensor:
     alias: "Tensor | None" = None                  # concat parent
     coff_in_alias: int = 0
     nchw_input: bool = False                       # the graph input (dense NCHW)
+    dtype: str = "f32"                             # "f32" | "bf16" element type of the buffer
 
     def root(self) -> tuple["Tensor", int]:
         t, off = self, 0
@@ -105,15 +106,18 @@ def _fold_bn(conv: nn.Conv2d, bn: nn.BatchNorm2d | None):
 
 
 class _Lowerer:
-    def __init__(self, gm: fx.GraphModule):
+    def __init__(self, gm: fx.GraphModule, dtype: str = "f32"):
         self.gm = gm
+        self.act_dtype = dtype          # element type of conv / pool activations
+        self.esize = 2 if dtype == "bf16" else 4
         self.ops: list[LoweredOp] = []
         self.tensors: list[Tensor] = []
         self.env: dict[fx.Node, Tensor] = {}
         self.consumed: set[fx.Node] = set()
 
-    def new_tensor(self, shape, producers=()):
-        t = Tensor(len(self.tensors), tuple(int(x) for x in shape), set(producers))
+    def new_tensor(self, shape, producers=(), dtype=None):
+        t = Tensor(len(self.tensors), tuple(int(x) for x in shape), set(producers),
+                   dtype=dtype or self.act_dtype)
         self.tensors.append(t)
         return t
 
@@ -171,7 +175,8 @@ class _Lowerer:
                        dict(N=n, H=h, W=w, Cin=cin, OH=oh, OW=ow, Cout=cout, R=r, S=s, sh=sh,
                             sw=sw, ph=ph, pw=pw, relu=int(relu_node is not None)),
                        [x], out, wk, b, flops=2 * macs,
-                       bytes_min=4 * (n * h * w * cin + wk.size + b.size + n * oh * ow * cout),
+                       bytes_min=(x.dtype == "bf16" and 2 or 4) * n * h * w * cin + self.esize * wk.size
+                       + 4 * b.size + self.esize * n * oh * ow * cout,
                        label=node.name)
         self.emit(op)
         self.env[tail] = out
@@ -191,16 +196,17 @@ class _Lowerer:
                        dict(N=n, H=h, W=w, C=c, OH=oh, OW=ow, kh=kh, kw=kw, sh=sh, sw=sw, ph=ph,
                             pw=pw, include_pad=int(include_pad)),
                        [x], out, flops=n * oh * ow * c * kh * kw,
-                       bytes_min=4 * (n * h * w * c + n * oh * ow * c), label=node.name)
+                       bytes_min=self.esize * (n * h * w * c + n * oh * ow * c), label=node.name)
         self.emit(op)
         self.env[node] = out
 
     def lower_gap(self, node):
         x = self.env[node.args[0]]
         n, h, w, c = x.shape
-        out = self.new_tensor((n, c))
+        out = self.new_tensor((n, c), dtype="f32")  # feeds the fp32 classifier head
         op = LoweredOp(GLOBAL_AVGPOOL, "pool", OpClass.MEMORY, dict(N=n, H=h, W=w, C=c), [x], out,
-                       flops=n * h * w * c, bytes_min=4 * (n * h * w * c + n * c), label=node.name)
+                       flops=n * h * w * c, bytes_min=self.esize * n * h * w * c + 4 * n * c,
+                       label=node.name)
         self.emit(op)
         self.env[node] = out
 
@@ -217,7 +223,9 @@ class _Lowerer:
             act = 1
             self.consumed.add(relu_node)
             tail = relu_node
-        out = self.new_tensor((m, nout))
+        if x.dtype != "f32":
+            raise LoweringError(f"{node.name}: the SIMT linear head expects fp32 rows")
+        out = self.new_tensor((m, nout), dtype="f32")
         wt = lin.weight.detach().float().cpu().contiguous().numpy()
         b = lin.bias.detach().float().cpu().numpy() if lin.bias is not None else None
         op = LoweredOp(LINEAR, "gemm", OpClass.COMPUTE, dict(M=m, K=k, N=nout, act=act), [x], out,
@@ -262,7 +270,7 @@ class _Lowerer:
                 if inp is not None:
                     raise LoweringError("single-input models only")
                 n, c, h, w = example.shape
-                inp = self.new_tensor((n, h, w, c))
+                inp = self.new_tensor((n, h, w, c), dtype="f32")
                 inp.nchw_input = True
                 self.env[node] = inp
             elif node.op == "output":
@@ -337,8 +345,14 @@ class _Lowerer:
         return Program(self.ops, self.tensors, inp, out, sorted(edges))
 
 
-def lower(model: nn.Module, example: torch.Tensor) -> Program:
-    """Trace `model` with torch.fx and lower it to executor operators."""
+def lower(model: nn.Module, example: torch.Tensor, dtype: str = "f32") -> Program:
+    """Trace `model` with torch.fx and lower it to executor operators.
+
+    dtype "f32": fp32 activations end to end (3xTF32 tensor-core convs).
+    dtype "bf16": bf16 activations and weights with fp32 accumulation; the
+    graph input stays fp32 NCHW and the classifier head stays fp32."""
+    if dtype not in ("f32", "bf16"):
+        raise ValueError(f"unknown dtype {dtype!r}")
     model = model.eval()
     gm = fx.symbolic_trace(model)
-    return _Lowerer(gm).run(example)
+    return _Lowerer(gm, dtype).run(example)

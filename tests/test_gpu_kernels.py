@@ -87,3 +87,32 @@ def test_conv_matches_torch(case, engine_name):
     # replaying twice is idempotent (split-K counters reset themselves)
     y2 = sg.run(x.cuda())
     assert torch.equal(y, y2)
+
+
+BF16_CASES = [
+    (64, 64, 1, 1, 0, 56),
+    (192, 96, 3, 1, 1, 28),
+    (160, 192, (1, 7), 1, (0, 3), 17),
+    (288, 384, 3, 2, 0, 35),
+    (2048, 320, 1, 1, 0, 8),
+    (12, 20, 3, 1, 1, 9),     # Cin % 8 != 0 -> register gather path
+]
+
+
+@pytest.mark.parametrize("case", BF16_CASES, ids=[str(c) for c in BF16_CASES])
+def test_conv_bf16_matches_torch(case):
+    """bf16 tcgen05 engine (kind::f16, fp32 accumulation) vs the fp64 module;
+    bf16 storage of inputs/weights/outputs bounds the error near 1e-2."""
+    from paper_2312_10351_b200 import engine
+    cin, cout, k, s, p, hw = case
+    torch.manual_seed(0)
+    m = Wrap(cin, cout, k, s, p, hw).eval()
+    x = torch.randn(1, 3, hw, hw)
+    sg = engine.compile(m, x, device=0, profile_reps=2, dtype="bf16")
+    assert all(engine.conv_engine_for(o, 1) == 2 for o in sg.program.ops if o.kind == 1)
+    y = sg.run(x.cuda())
+    with torch.no_grad():
+        ref = m.double()(x.double())
+    y_nchw = y.permute(0, 3, 1, 2).float().cpu()
+    assert _rel(y_nchw, ref) < 1.5e-2
+    assert torch.equal(sg.run(x.cuda()), y)
