@@ -162,16 +162,24 @@ def run_gpu(args) -> dict | None:
     from paper_2312_10351_b200 import engine, zoo
     from paper_2312_10351_b200.dag import graph_to_dict
 
-    model, x = zoo.build(args.model)
+    if args.model == "bert_base":
+        model, ref_model, x = zoo.build_bert()
+        args.dtype = "bf16"  # BASELINE config: BERT-base seq 128 bf16
+    else:
+        model, x = zoo.build(args.model)
+        ref_model = model
     sg = engine.compile(model, x, device=local, bound_grids=args.bounded, profile_reps=args.profile_reps,
                         dtype=args.dtype)
     xd = x.cuda(local)
     # correctness guard on every rank: a fast wrong answer is not a result
     y = sg.run(xd)
+    y = y[0] if isinstance(y, tuple) else y
     with torch.no_grad():
-        ref = model.cuda(local)(xd)
+        ref = ref_model.cuda(local)(xd)
+    ref = ref[0] if isinstance(ref, tuple) else ref
+    y = y.float().reshape(ref.shape)
     rel = (torch.linalg.vector_norm(y - ref) / torch.linalg.vector_norm(ref)).item()
-    model.cpu()
+    ref_model.cpu()
     del ref
     torch.cuda.synchronize()
 
@@ -219,16 +227,19 @@ def run_gpu(args) -> dict | None:
         if op.kind == 0:
             continue
         if op.kind == 1:
-            name = "conv2d_tc_tf32x3" if engine.conv_engine_for(op, sg.conv_engine) == 1 else "conv2d_f32_simt"
+            name = {0: "conv2d_f32_simt", 1: "conv2d_tc_tf32x3", 2: "conv2d_tc_bf16"}[
+                engine.conv_engine_for(op, sg.conv_engine)]
         else:
-            name = {2: "maxpool2d", 3: "avgpool2d", 4: "global_avgpool", 5: "linear_f32"}[op.kind]
+            name = {2: "maxpool2d", 3: "avgpool2d", 4: "global_avgpool", 5: "linear_f32", 7: "layernorm",
+                    9: "embedding", 10: "attention_tc"}[op.kind]
         f = fam.setdefault(name, {"us": 0.0, "flops": 0, "bytes": 0, "launches": 0})
         f["us"] += p["isolated_us"]
         f["flops"] += op.flops
         f["bytes"] += op.bytes_min
         f["launches"] += 1
     peak_of = {"conv2d_tc_tf32x3": tc_peak_tflops, "conv2d_f32_simt": FP32_SIMT_NOMINAL_TFLOPS,
-               "linear_f32": FP32_SIMT_NOMINAL_TFLOPS}
+               "linear_f32": FP32_SIMT_NOMINAL_TFLOPS, "conv2d_tc_bf16": peaks["bf16_tflops"],
+               "attention_tc": peaks["bf16_tflops"]}
     # DAG roofline: max(critical path, FLOPs at compute peak + bytes at HBM peak)
     flop_term_us = sum(f["flops"] / (peak_of.get(k, FP32_SIMT_NOMINAL_TFLOPS) * 1e12) * 1e6
                        for k, f in fam.items() if k in peak_of)
@@ -262,6 +273,7 @@ def run_gpu(args) -> dict | None:
         "unit": unit, "frac": round(achieved / peak, 4),
         "peak_source": ("measured bf16 (MEASURED_PEAKS.json) / 2 (tf32 rate) / 3 (3xTF32 passes)"
                         if dom == "conv2d_tc_tf32x3" else
+                        "measured bf16 dense (MEASURED_PEAKS.json)" if dom in ("conv2d_tc_bf16", "attention_tc") else
                         "nominal fp32 FFMA (148 SM x 128 lanes x 2 x 1.965 GHz)" if unit == "TFLOP/s"
                         else "measured HBM copy (MEASURED_PEAKS.json)"),
         "traffic": traffic,
@@ -389,7 +401,7 @@ def main(argv=None) -> int:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--model", default="inception_v3", choices=["inception_v3", "googlenet"])
+    ap.add_argument("--model", default="inception_v3", choices=["inception_v3", "googlenet", "bert_base"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])

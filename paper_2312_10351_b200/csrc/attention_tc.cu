@@ -1,0 +1,209 @@
+// Multi-head self-attention for one sequence, one CTA per head, on tcgen05:
+//   S = Q K^T          (tcgen05.mma kind::f16, M = 128 queries, N = 128 keys, K = 64)
+//   P = exp((S - max) * scale)   rows in registers straight from TMEM (tcgen05.ld)
+//   O = P V / rowsum   (tcgen05.mma, M = 128 queries, N = 64, K = 128 keys)
+// Q, K, V and O are channel views of [tokens][C] bf16 buffers (head h reads
+// columns off + h*64 ..); S and O accumulate in TMEM (fp32).  Operands are
+// staged in 64-byte-swizzled K-major atoms (Q, K by cp.async; V transposed on
+// the way in so the PV MMA reads K-major V^T; P written by the softmax warps).
+// Shapes: tokens = 128, head_dim = 64 (BERT-base at seq 128).
+
+#include <cuda_bf16.h>
+
+#include "device_common.cuh"
+#include "ops.h"
+#include "status.h"
+#include "tc_common.cuh"
+
+namespace opara {
+namespace {
+
+constexpr int kT = 128, kD = 64, kThreads = 128;
+constexpr uint32_t kQBytes = kT * kD * 2, kKBytes = kT * kD * 2, kPBytes = kT * kT * 2, kVBytes = kD * kT * 2;
+
+struct AttnArgs {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  __nv_bfloat16* out;
+  int q_stride, k_stride, v_stride, out_stride;
+  int q_off, k_off, v_off, out_off;
+  float scale;
+};
+
+// Byte offset of 16-byte chunk `c16` (8 bf16 along K) of `row` in a SW64
+// K-major operand with `rows` rows: K is split into 32-element blocks of
+// rows * 64 B, each an array of 8-row x 64 B swizzle atoms.
+__device__ __forceinline__ uint32_t sw64(int rows, int row, int c16) {
+  const int kb = c16 >> 2, cw = c16 & 3, r8 = row & 7;
+  return static_cast<uint32_t>(kb * rows * 64 + (row >> 3) * 512 + r8 * 64 + ((cw ^ ((r8 >> 1) & 3)) << 4));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned long long* trace) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* qs = smem;
+  uint8_t* ks = qs + kQBytes;
+  uint8_t* ps = ks + kKBytes;
+  uint8_t* vt = ps + kPBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vt + kVBytes);  // [0] S ready, [1] O ready
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+
+  pdl_trigger();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int h = blockIdx.x;
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, 256);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tS = tmem, tO = tmem + 128;
+
+  pdl_wait();
+  trace_begin(trace);
+  // ---- stage Q, K (cp.async) and V^T (register transpose)
+  const __nv_bfloat16* qg = a.q + a.q_off + h * kD;
+  const __nv_bfloat16* kg = a.k + a.k_off + h * kD;
+  const __nv_bfloat16* vg = a.v + a.v_off + h * kD;
+  for (int u = tid; u < kT * (kD / 8); u += kThreads) {
+    const int row = u >> 3, c16 = u & 7;
+    cp_async16(tc::smem_u32(qs) + sw64(kT, row, c16), qg + static_cast<int64_t>(row) * a.q_stride + c16 * 8);
+    cp_async16(tc::smem_u32(ks) + sw64(kT, row, c16), kg + static_cast<int64_t>(row) * a.k_stride + c16 * 8);
+  }
+  for (int u = tid; u < kT * (kD / 8); u += kThreads) {
+    const int key = u >> 3, d0 = (u & 7) * 8;
+    const uint4 raw = *reinterpret_cast<const uint4*>(vg + static_cast<int64_t>(key) * a.v_stride + d0);
+    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)  // V^T[d][key]: row d, k = key
+      *reinterpret_cast<__nv_bfloat16*>(vt + sw64(kD, d0 + i, key >> 3) + (key & 7) * 2) = e[i];
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  tc::fence_proxy_async_smem();
+  __syncthreads();
+
+  // ---- S = Q K^T
+  constexpr uint32_t kIdS = tc::instr_desc(1, 128, 128);
+  constexpr uint32_t kIdO = tc::instr_desc(1, 128, 64);
+  if (tid == 0) {
+    tc::tc_fence_after();
+#pragma unroll
+    for (int s = 0; s < kD / 16; ++s) {
+      const uint32_t off = (s >> 1) * kT * 64 + (s & 1) * 32;
+      tc::mma_f16(tS, tc::smem_desc_sw64(tc::smem_u32(qs) + off, 512),
+                  tc::smem_desc_sw64(tc::smem_u32(ks) + off, 512), kIdS, s != 0);
+    }
+    tc::mma_commit(&bar[0]);
+  }
+  tc::mbar_wait(&bar[0], 0);
+  tc::tc_fence_after();
+
+  // ---- softmax: thread = query row (TMEM lane), 128 scores in registers
+  const int q = warp * 32 + lane;
+  const uint32_t trow = static_cast<uint32_t>(warp * 32) << 16;
+  float sc[kT];
+#pragma unroll
+  for (int c8 = 0; c8 < kT / 8; ++c8) {
+    float v[8];
+    tc::tmem_ld8(tS + trow + c8 * 8, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sc[c8 * 8 + e] = v[e];
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < kT; ++j) mx = fmaxf(mx, sc[j]);
+  float sum = 0.f;
+#pragma unroll
+  for (int c16 = 0; c16 < kT / 8; ++c16) {
+    __nv_bfloat16 pv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float p = __expf((sc[c16 * 8 + e] - mx) * a.scale);
+      const __nv_bfloat16 pb = __float2bfloat16_rn(p);
+      sum += __bfloat162float(pb);  // normalise by exactly what the PV MMA consumes
+      pv[e] = pb;
+    }
+    *reinterpret_cast<uint4*>(ps + sw64(kT, q, c16)) = *reinterpret_cast<const uint4*>(pv);
+  }
+  tc::fence_proxy_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+
+  // ---- O = P V
+  if (tid == 0) {
+    tc::tc_fence_after();
+#pragma unroll
+    for (int s = 0; s < kT / 16; ++s) {
+      tc::mma_f16(tO, tc::smem_desc_sw64(tc::smem_u32(ps) + (s >> 1) * kT * 64 + (s & 1) * 32, 512),
+                  tc::smem_desc_sw64(tc::smem_u32(vt) + (s >> 1) * kD * 64 + (s & 1) * 32, 512), kIdO, s != 0);
+    }
+    tc::mma_commit(&bar[1]);
+  }
+  tc::mbar_wait(&bar[1], 0);
+  tc::tc_fence_after();
+  const float inv = 1.f / sum;
+  __nv_bfloat16* og = a.out + static_cast<int64_t>(q) * a.out_stride + a.out_off + h * kD;
+#pragma unroll
+  for (int c8 = 0; c8 < kD / 8; ++c8) {
+    float v[8];
+    tc::tmem_ld8(tO + trow + c8 * 8, v);
+    __nv_bfloat16 ob[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ob[e] = __float2bfloat16_rn(v[e] * inv);
+    *reinterpret_cast<uint4*>(og + c8 * 8) = *reinterpret_cast<const uint4*>(ob);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 256);
+  }
+  trace_end(trace);
+}
+
+}  // namespace
+
+// ATTENTION  i: 0 tokens (128), 1 heads, 2 head_dim (64), 3 q_stride, 4 k_stride, 5 v_stride,
+//               6 out_stride, 7 q_off, 8 k_off, 9 v_off, 10 out_off;  f[0] scale
+//            p: 0 q, 1 k, 2 v, 3 out (bf16 [tokens][stride] buffers)
+opara_status launch_attention(const opara_op& op, cudaStream_t s, unsigned long long* trace, LaunchCfg* cfg,
+                              bool dry) {
+  if (op.i[0] != kT || op.i[2] != kD)
+    return fail(OPARA_ERR_VALUE, "attention_tc: tokens must be 128 and head_dim 64");
+  AttnArgs a;
+  a.q = static_cast<const __nv_bfloat16*>(op.p[0]);
+  a.k = static_cast<const __nv_bfloat16*>(op.p[1]);
+  a.v = static_cast<const __nv_bfloat16*>(op.p[2]);
+  a.out = static_cast<__nv_bfloat16*>(op.p[3]);
+  a.q_stride = (int)op.i[3]; a.k_stride = (int)op.i[4]; a.v_stride = (int)op.i[5]; a.out_stride = (int)op.i[6];
+  a.q_off = (int)op.i[7]; a.k_off = (int)op.i[8]; a.v_off = (int)op.i[9]; a.out_off = (int)op.i[10];
+  a.scale = static_cast<float>(op.f[0]);
+  for (int x : {a.q_stride, a.k_stride, a.v_stride, a.out_stride, a.q_off, a.k_off, a.v_off, a.out_off})
+    if (x % 8) return fail(OPARA_ERR_VALUE, "attention_tc: strides/offsets must be multiples of 8");
+  LaunchCfg c;
+  c.func = reinterpret_cast<const void*>(&attention_tc);
+  c.grid = dim3(static_cast<unsigned>(op.i[1]));
+  c.block = dim3(kThreads);
+  c.smem = kQBytes + kKBytes + kPBytes + kVBytes + 64 + 1024;
+  if (cfg) *cfg = c;
+  if (dry) return OPARA_OK;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(c.func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
+    if (e != cudaSuccess) return cuda_fail(e, "attention_tc smem attribute");
+    attr = true;
+  }
+  void* args[] = {&a, &trace};
+  return launch_kernel(c, args, s);
+}
+
+}  // namespace opara

@@ -50,9 +50,9 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   constexpr int B_PER = BK * BN / T;
   __shared__ __align__(16) float As[2][BK][BM + 4];
   __shared__ __align__(16) float Bs[2][BK][BN + 4];
-  trace_begin(trace);
   pdl_trigger();
   pdl_wait();
+  trace_begin(trace);  // timeline starts once the inputs are ready (after the PDL wait)
 
   const int tid = threadIdx.x;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;

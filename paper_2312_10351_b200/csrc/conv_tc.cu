@@ -109,7 +109,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   uint64_t* accum = landed + kStages;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(accum + 1);
 
-  trace_begin(trace);
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool dbg = a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
@@ -184,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
         dq = rs - dr * a.S;
       }
       pdl_wait();  // the input activations come from the predecessor grid
+      trace_begin(trace);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);

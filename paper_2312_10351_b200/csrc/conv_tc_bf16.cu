@@ -86,7 +86,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   uint64_t* accum = empty + kStages;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(accum + 1);
 
-  trace_begin(trace);
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n0 = blockIdx.x * BN;
@@ -132,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       }
     }
     pdl_wait();
+    trace_begin(trace);
     if constexpr (kMode == kVecBf16) {
       const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(a.in);
       const __nv_bfloat16* rowbase[kRowsPerThread];

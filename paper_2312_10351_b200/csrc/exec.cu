@@ -76,6 +76,9 @@ opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* t
     case OPARA_OP_AVGPOOL2D: return launch_pool2d(op, s, trace, cfg, dry);
     case OPARA_OP_GLOBAL_AVGPOOL: return launch_global_avgpool(op, s, trace, cfg, dry);
     case OPARA_OP_LINEAR: return launch_linear(op, s, trace, cfg, dry);
+    case OPARA_OP_LAYERNORM:
+    case OPARA_OP_EMBEDDING: return launch_rows(op, s, trace, cfg, dry);
+    case OPARA_OP_ATTENTION: return launch_attention(op, s, trace, cfg, dry);
     default: return fail(OPARA_ERR_VALUE, "unsupported op kind " + std::to_string(op.kind));
   }
 }

@@ -30,9 +30,9 @@ __device__ __forceinline__ float activate(float v, int act) {
 
 template <int kRows, bool kVec>
 __global__ void __launch_bounds__(256) linear_rows_f32(LinArgs a, unsigned long long* trace) {
-  trace_begin(trace);
   pdl_trigger();
   pdl_wait();
+  trace_begin(trace);  // timeline starts once the inputs are ready (after the PDL wait)
   const int lane = threadIdx.x & 31;
   const int warps_per_block = blockDim.x / 32;
   const int row_groups = (a.M + kRows - 1) / kRows;

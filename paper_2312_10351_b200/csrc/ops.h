@@ -63,6 +63,8 @@ opara_status launch_pool2d(const opara_op&, cudaStream_t, unsigned long long*, L
 opara_status launch_global_avgpool(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*,
                                    bool);
 opara_status launch_linear(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+opara_status launch_rows(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+opara_status launch_attention(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
 
 // Dispatch on op.kind.
 opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* trace,

@@ -37,9 +37,9 @@ template <bool kMax, int V, typename T>
 __global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long long* trace) {
   const T* in = static_cast<const T*>(a.in);
   T* outp = static_cast<T*>(a.out);
-  trace_begin(trace);
   pdl_trigger();
   pdl_wait();
+  trace_begin(trace);  // timeline starts once the inputs are ready (after the PDL wait)
   const int cv = a.C / V;
   const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -110,9 +110,9 @@ __global__ void __launch_bounds__(256) global_avgpool_nhwc(const T* __restrict__
                                                            float* __restrict__ out, int N, int HW,
                                                            int C, int in_cs, int in_coff,
                                                            unsigned long long* trace) {
-  trace_begin(trace);
   pdl_trigger();
   pdl_wait();
+  trace_begin(trace);  // timeline starts once the inputs are ready (after the PDL wait)
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
   const int64_t total = static_cast<int64_t>(N) * C;
@@ -137,9 +137,9 @@ __global__ void __launch_bounds__(128) global_avgpool_nhwc_cols(const T* __restr
                                                                 int HW, int C, int in_cs,
                                                                 int in_coff,
                                                                 unsigned long long* trace) {
-  trace_begin(trace);
   pdl_trigger();
   pdl_wait();
+  trace_begin(trace);  // timeline starts once the inputs are ready (after the PDL wait)
   const int64_t total = static_cast<int64_t>(N) * C;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {

@@ -31,7 +31,8 @@ import torch
 from . import _lib
 from .dag import ComputationGraph, OperatorNode, ResourceDemand, graph_to_dict
 from .device import GpuConfig, device_gpu_config, GPU_PRESETS
-from .frontend import (AVGPOOL2D, CONV2D, GLOBAL_AVGPOOL, LINEAR, MAXPOOL2D, NOP, Program, lower)
+from .frontend import (ATTENTION, AVGPOOL2D, CONV2D, EMBEDDING, GLOBAL_AVGPOOL, LAYERNORM, LINEAR, MAXPOOL2D,
+                       NOP, Program, lower)
 from .order import LaunchSchedule, make_order
 from .plan import StreamPlan, allocate_streams, plan_to_dict, single_stream_plan
 
@@ -164,6 +165,8 @@ def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -
     rec.variant = -1
     if op.kind == NOP:
         return rec
+    if op.kind in (LAYERNORM, EMBEDDING, ATTENTION):
+        return _row_record(rec, op, views, weights)
     q = op.ints
     (ib, icoff, ics, inchw), (ob, ocoff, ocs) = views
     i = rec.i
@@ -189,6 +192,34 @@ def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -
         raise ValueError(f"unknown op kind {op.kind}")
     for k, v in enumerate(vals):
         i[k] = int(v)
+    return rec
+
+
+def _row_record(rec, op, views, arrays):
+    """Records of the transformer row kernels (layouts: csrc/norm.cu, attention_tc.cu).
+    `views` = [(ptr, coff, cstride, ...)] for the inputs then the output;
+    `arrays` = device pointers of op.arrays by name."""
+    q = op.ints
+    *ins, (ob, ocoff, ocs) = views
+    esize = 2 if op.output.dtype == "bf16" else 4
+    if op.kind == EMBEDDING:
+        vals = [q["rows"], q["C"], 0, 0, ocs, 0]
+        rec.p[0], rec.p[1] = ins[0][0], None
+        rec.p[2], rec.p[3], rec.p[4] = arrays["gamma"], arrays["beta"], ob + esize * ocoff
+        rec.p[5], rec.p[6], rec.p[7] = arrays["word"], arrays["pos"], arrays["type"]
+    elif op.kind == LAYERNORM:
+        (ab, acoff, acs, _), (bb, bcoff, bcs, _) = ins
+        vals = [q["rows"], q["C"], acs, bcs, ocs, 0]
+        rec.p[0], rec.p[1] = ab + esize * acoff, bb + esize * bcoff
+        rec.p[2], rec.p[3], rec.p[4] = arrays["gamma"], arrays["beta"], ob + esize * ocoff
+    else:  # ATTENTION
+        (qb, qo, qs, _), (kb, ko, ks, _), (vb, vo, vs, _) = ins
+        vals = [q["T"], q["heads"], q["C"] // q["heads"], qs, ks, vs, ocs, qo, ko, vo, ocoff]
+        rec.p[0], rec.p[1], rec.p[2], rec.p[3] = qb, kb, vb, ob
+    for k, v in enumerate(vals):
+        rec.i[k] = int(v)
+    for k, v in enumerate(op.floats):
+        rec.f[k] = float(v)
     return rec
 
 
@@ -218,8 +249,11 @@ class ScheduledGraph:
         recs = (_lib.OparaOp * len(program.ops))()
         self.targets = concurrency_targets(program) if bound_grids else {}
         for k, op in enumerate(program.ops):
-            recs[k] = _op_record(op, self._views(op), self._weights(op),
-                                 conv_engine_for(op, self.conv_engine), self.targets.get(k, 0))
+            if op.kind in (LAYERNORM, EMBEDDING, ATTENTION):
+                recs[k] = _op_record(op, self._all_views(op), self._arrays(op))
+            else:
+                recs[k] = _op_record(op, self._views(op), self._weights(op),
+                                     conv_engine_for(op, self.conv_engine), self.targets.get(k, 0))
         self.debug_ts = {}
         if os.environ.get("OPARA_CONV_DEBUG"):  # per-phase timestamps of CTA 0 (conv_tc.cu)
             for k, op in enumerate(program.ops):
@@ -248,7 +282,7 @@ class ScheduledGraph:
         for t in program.tensors:
             if t.alias is not None:
                 continue
-            tdt = torch.bfloat16 if t.dtype == "bf16" else torch.float32
+            tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "i64": torch.int64}[t.dtype]
             if t.nchw_input:
                 n, h, w, c = t.shape
                 buf = torch.zeros((n, c, h, w), dtype=tdt, device=self.dev)
@@ -257,10 +291,13 @@ class ScheduledGraph:
             self._bufs[t.tid] = buf
         root, _ = program.input.root()
         self.input_buffer = self._bufs[root.tid]
-        oroot, ooff = program.output.root()
-        if ooff != 0 or oroot.shape != program.output.shape:
-            raise RuntimeError("graph output must be a whole buffer")
-        self.output_buffer = self._bufs[oroot.tid]
+        self.output_buffers = []
+        for out in (program.outputs or [program.output]):
+            oroot, ooff = out.root()
+            if ooff != 0 or oroot.shape != out.shape:
+                raise RuntimeError("graph outputs must be whole buffers")
+            self.output_buffers.append(self._bufs[oroot.tid])
+        self.output_buffer = self.output_buffers[0]
 
     def _views(self, op):
         x = op.inputs[0]
@@ -270,6 +307,23 @@ class ScheduledGraph:
         ob = self._bufs[out_r.tid]
         return ((xb.data_ptr(), xoff, xr.shape[-1], xr.nchw_input),
                 (ob.data_ptr(), out_off, out_r.shape[-1]))
+
+    def _all_views(self, op):
+        out = []
+        for t in op.inputs:
+            r, off = t.root()
+            out.append((self._bufs[r.tid].data_ptr(), off, r.shape[-1], r.nchw_input))
+        r, off = op.output.root()
+        out.append((self._bufs[r.tid].data_ptr(), off, r.shape[-1]))
+        return out
+
+    def _arrays(self, op):
+        ptrs = {}
+        for name, arr in op.arrays.items():
+            t = torch.from_numpy(np.ascontiguousarray(arr)).to(self.dev)
+            self._keep.append(t)
+            ptrs[name] = t.data_ptr()
+        return ptrs
 
     def _weights(self, op):
         ptrs = []
@@ -324,11 +378,13 @@ class ScheduledGraph:
         s = stream or torch.cuda.current_stream(self.dev)
         _lib.check(_lib.lib().opara_exec_replay(self._h, slot, C.c_void_p(s.cuda_stream)))
 
-    def run(self, x: torch.Tensor, slot: int = SLOT_PARALLEL) -> torch.Tensor:
-        """One inference: copy `x` (NCHW) in, replay, return a copy of the output."""
-        self.input_buffer.copy_(x, non_blocking=True)
+    def run(self, x: torch.Tensor, slot: int = SLOT_PARALLEL):
+        """One inference: copy `x` in (NCHW image or [1, T] token ids), replay,
+        return a copy of the output (a tuple when the model has several)."""
+        self.input_buffer.copy_(x.reshape(self.input_buffer.shape), non_blocking=True)
         self.replay(slot)
-        return self.output_buffer.clone()
+        outs = tuple(b.clone() for b in self.output_buffers)
+        return outs[0] if len(outs) == 1 else outs
 
     def run_host(self, x_host: torch.Tensor, out_host: torch.Tensor, slot: int = SLOT_PARALLEL) -> None:
         """Host-buffer inference (asynchronous): H2D copy of `x_host` (pinned
@@ -340,7 +396,7 @@ class ScheduledGraph:
     def time_host_roundtrip(self, x: torch.Tensor, warmup: int = 10, iters: int = 100,
                             slot: int = SLOT_PARALLEL) -> dict:
         """Time run_host end to end (CUDA events bracketing H2D + replay + D2H)."""
-        x_host = x.detach().to(torch.float32).contiguous().pin_memory()
+        x_host = x.detach().to(self.input_buffer.dtype).reshape(self.input_buffer.shape).contiguous().pin_memory()
         out_host = torch.empty(self.output_buffer.shape, dtype=self.output_buffer.dtype).pin_memory()
         s = torch.cuda.current_stream(self.dev)
         for _ in range(warmup):
@@ -455,12 +511,16 @@ def static_dag(program: Program, gpu_config: GpuConfig | None = None,
     cfg = gpu_config or GPU_PRESETS["b200"]
     targets = concurrency_targets(program) if bound_grids else {}
     nodes = []
-    dummy = []
     for k, op in enumerate(program.ops):
-        views = ((0x1000, 0, op.inputs[0].root()[0].shape[-1], op.inputs[0].root()[0].nchw_input),
-                 (0x2000, op.output.root()[1], op.output.root()[0].shape[-1]))
-        rec = _op_record(op, views, (0x3000, 0x4000), conv_engine_for(op, CONV_ENGINES[conv_engine]),
-                         targets.get(k, 0))
+        if op.kind in (LAYERNORM, EMBEDDING, ATTENTION):
+            views = [(0x1000 * (j + 1), t.root()[1], t.root()[0].shape[-1], False) for j, t in enumerate(op.inputs)]
+            views.append((0x9000, op.output.root()[1], op.output.root()[0].shape[-1]))
+            rec = _op_record(op, views, {name: 0xA000 for name in op.arrays})
+        else:
+            views = ((0x1000, 0, op.inputs[0].root()[0].shape[-1], op.inputs[0].root()[0].nchw_input),
+                     (0x2000, op.output.root()[1], op.output.root()[0].shape[-1]))
+            rec = _op_record(op, views, (0x3000, 0x4000), conv_engine_for(op, CONV_ENGINES[conv_engine]),
+                             targets.get(k, 0))
         prof = _lib.OparaOpProfile()
         _lib.check(_lib.lib().opara_op_launch_config(C.byref(rec), C.byref(prof)))
         d = ResourceDemand(prof.threads_per_block, prof.shared_mem_per_block,

@@ -28,6 +28,7 @@ from .dag import OpClass
 
 # opara_op_kind values (include/opara.h)
 NOP, CONV2D, MAXPOOL2D, AVGPOOL2D, GLOBAL_AVGPOOL, LINEAR = 0, 1, 2, 3, 4, 5
+LAYERNORM, EMBEDDING, ATTENTION = 7, 9, 10
 
 
 @dataclass
@@ -64,6 +65,8 @@ class LoweredOp:
     flops: int = 0            # algorithmic FLOPs (2*MAC for conv/linear)
     bytes_min: int = 0        # algorithmic bytes: inputs read once + weights + output written
     label: str = ""           # fx node name, for reports
+    arrays: dict = field(default_factory=dict)  # extra host arrays (tables, LN affine)
+    floats: tuple = ()        # float parameters (eps, scale)
 
 
 class LoweringError(RuntimeError):
@@ -75,8 +78,9 @@ class Program:
     ops: list
     tensors: list
     input: Tensor
-    output: Tensor
+    output: Tensor            # first graph output
     edges: list               # (u, v) op indices
+    outputs: list = field(default_factory=list)
 
 
 def _pool_out(size, k, s, p, ceil_mode):
@@ -257,11 +261,94 @@ class _Lowerer:
         self.emit(LoweredOp(NOP, "concat", OpClass.MEMORY, {}, ins, out, label=node.name))
         self.env[node] = out
 
+    # ------------------------------------------------- transformer rows path
+    # Token activations are [T, C] row blocks stored as (1, 1, T, C) channel
+    # views, so a linear layer is a 1x1 conv over T "pixels".
+
+    def _param(self, node):
+        if not (isinstance(node, fx.Node) and node.op == "get_attr"):
+            raise LoweringError(f"{node}: expected a parameter (get_attr)")
+        obj = self.gm
+        for part in node.target.split("."):
+            obj = getattr(obj, part)
+        return obj.detach().float().cpu()
+
+    def lower_linear_rows(self, node):
+        x = self.env[node.args[0]]
+        w = self._param(node.args[1])
+        b = self._param(node.args[2]) if len(node.args) > 2 and node.args[2] is not None else None
+        n, h, t, k = x.shape
+        nout = w.shape[0]
+        tail, act = node, 0
+        for pred_fn, code in ((lambda u: u.op == "call_function" and u.target is F.gelu, 2),
+                              (lambda u: u.op == "call_function" and u.target is torch.tanh, 3),
+                              (self._is_relu, 1)):
+            nxt = self._single_user(node, pred_fn)
+            if nxt is not None:
+                if code == 2 and nxt.kwargs.get("approximate", "none") != "none":
+                    continue
+                tail, act = nxt, code
+                self.consumed.add(nxt)
+                break
+        out = self.new_tensor((1, 1, t, nout))
+        bias = (b if b is not None else torch.zeros(nout)).numpy()
+        op = LoweredOp(CONV2D, "gemm", OpClass.COMPUTE,
+                       dict(N=1, H=1, W=t, Cin=k, OH=1, OW=t, Cout=nout, R=1, S=1, sh=1, sw=1, ph=0, pw=0,
+                            relu=int(act == 1), act=act),
+                       [x], out, w.t().contiguous().numpy(), bias, flops=2 * t * k * nout,
+                       bytes_min=self.esize * (t * k + k * nout + t * nout) + 4 * nout, label=node.name)
+        self.emit(op)
+        self.env[tail] = out
+
+    def lower_embeddings(self, node):
+        ids = self.env[node.args[0]]
+        word, pos, typ, gamma, beta = (self._param(a) for a in node.args[1:6])
+        eps = float(node.args[6])
+        t, c = ids.shape[-1], word.shape[1]
+        out = self.new_tensor((1, 1, t, c))
+        op = LoweredOp(EMBEDDING, "embedding", OpClass.MEMORY, dict(rows=t, C=c), [ids], out,
+                       flops=8 * t * c, bytes_min=8 * t + 3 * 4 * t * c + self.esize * t * c, label=node.name,
+                       arrays={"gamma": gamma.numpy(), "beta": beta.numpy(), "word": word.numpy(),
+                               "pos": pos.numpy(), "type": typ.numpy()}, floats=(eps,))
+        self.emit(op)
+        self.env[node] = out
+
+    def lower_attention(self, node):
+        q, k, v = (self.env[a] for a in node.args[:3])
+        heads = int(node.args[3])
+        t, c = q.shape[2], q.shape[3]
+        out = self.new_tensor((1, 1, t, c))
+        op = LoweredOp(ATTENTION, "attention", OpClass.COMPUTE, dict(T=t, C=c, heads=heads), [q, k, v], out,
+                       flops=4 * t * t * c, bytes_min=self.esize * 4 * t * c, label=node.name,
+                       floats=((c // heads) ** -0.5,))
+        self.emit(op)
+        self.env[node] = out
+
+    def lower_add_layernorm(self, node):
+        x, r = self.env[node.args[0]], self.env[node.args[1]]
+        gamma, beta = self._param(node.args[2]), self._param(node.args[3])
+        eps = float(node.args[4])
+        t, c = x.shape[2], x.shape[3]
+        out = self.new_tensor((1, 1, t, c))
+        op = LoweredOp(LAYERNORM, "layernorm", OpClass.MEMORY, dict(rows=t, C=c), [x, r], out,
+                       flops=8 * t * c, bytes_min=self.esize * 3 * t * c, label=node.name,
+                       arrays={"gamma": gamma.numpy(), "beta": beta.numpy()}, floats=(eps,))
+        self.emit(op)
+        self.env[node] = out
+
+    def lower_first_token(self, node):
+        x = self.env[node.args[0]]
+        view = self.new_tensor((1, 1, 1, x.shape[3]), dtype=x.dtype)
+        view.alias, view.coff_in_alias = x, 0   # pixel 0 of x's buffer: a shorter view
+        view.producers = set(x.producers)
+        self.env[node] = view
+
     # ------------------------------------------------------------- driver
 
     def run(self, example: torch.Tensor) -> Program:
-        if example.dim() != 4:
-            raise LoweringError("example input must be a 4-D NCHW tensor")
+        token_input = example.dim() == 2 and not example.is_floating_point()
+        if example.dim() != 4 and not token_input:
+            raise LoweringError("example input must be a 4-D NCHW image or a [1, T] token-id tensor")
         inp = None
         for node in self.gm.graph.nodes:
             if node in self.consumed:
@@ -269,15 +356,19 @@ class _Lowerer:
             if node.op == "placeholder":
                 if inp is not None:
                     raise LoweringError("single-input models only")
-                n, c, h, w = example.shape
-                inp = self.new_tensor((n, h, w, c), dtype="f32")
-                inp.nchw_input = True
+                if token_input:
+                    inp = self.new_tensor(tuple(example.shape), dtype="i64")
+                else:
+                    n, c, h, w = example.shape
+                    inp = self.new_tensor((n, h, w, c), dtype="f32")
+                    inp.nchw_input = True
                 self.env[node] = inp
+            elif node.op == "get_attr":
+                self.env[node] = None  # parameters are read where they are consumed
             elif node.op == "output":
                 res = node.args[0]
-                if isinstance(res, (tuple, list)):
-                    res = res[0]
-                self.env["__out__"] = self.env[res]
+                outs = list(res) if isinstance(res, (tuple, list)) else [res]
+                self.env["__outs__"] = [self.env[r] for r in outs]
             elif node.op == "call_module":
                 mod = self.gm.get_submodule(node.target)
                 if isinstance(mod, nn.Conv2d):
@@ -302,8 +393,19 @@ class _Lowerer:
                     raise LoweringError(f"{node.name}: unsupported module {type(mod).__name__}")
             elif node.op == "call_function":
                 tgt = node.target
+                name = getattr(tgt, "__name__", "")
                 if tgt is torch.cat:
                     self.lower_cat(node)
+                elif tgt is F.linear:
+                    self.lower_linear_rows(node)
+                elif name == "bert_embeddings":
+                    self.lower_embeddings(node)
+                elif name == "self_attention":
+                    self.lower_attention(node)
+                elif name == "add_layer_norm":
+                    self.lower_add_layernorm(node)
+                elif name == "first_token":
+                    self.lower_first_token(node)
                 elif tgt is torch.flatten:
                     x = self.env[node.args[0]]
                     if len(x.shape) == 2:
@@ -336,13 +438,16 @@ class _Lowerer:
                     raise LoweringError(f"{node.name}: unsupported function {tgt}")
             else:
                 raise LoweringError(f"{node.name}: unsupported fx op {node.op}")
-        out = self.env["__out__"]
+        outs = self.env["__outs__"]
+        for t in outs:  # graph outputs leave the GEMM engine in fp32
+            if t.producers and self.ops[min(t.producers)].kind == CONV2D and t.alias is None:
+                t.dtype = "f32"
         edges = set()
         for v, op in enumerate(self.ops):
             for t in op.inputs:
                 for u in t.producers:
                     edges.add((u, v))
-        return Program(self.ops, self.tensors, inp, out, sorted(edges))
+        return Program(self.ops, self.tensors, inp, outs[0], sorted(edges), outs)
 
 
 def lower(model: nn.Module, example: torch.Tensor, dtype: str = "f32") -> Program:

@@ -116,3 +116,38 @@ def test_conv_bf16_matches_torch(case):
     y_nchw = y.permute(0, 3, 1, 2).float().cpu()
     assert _rel(y_nchw, ref) < 1.5e-2
     assert torch.equal(sg.run(x.cuda()), y)
+
+
+def test_attention_and_layernorm_rows():
+    """One BERT layer in isolation (embedding, Q/K/V GEMMs, tcgen05 attention,
+    residual LayerNorm) vs the torch restatement in fp64."""
+    import torch.nn.functional as F
+    from paper_2312_10351_b200 import engine, zoo
+    from transformers import BertConfig, BertModel
+
+    class OneLayer(torch.nn.Module):
+        def __init__(self, hf):
+            super().__init__()
+            self.hf = hf
+
+        def forward(self, ids):
+            e = self.hf.embeddings
+            x = zoo.bert_embeddings(ids, e.word_embeddings.weight, e.position_embeddings.weight,
+                                    e.token_type_embeddings.weight, e.LayerNorm.weight, e.LayerNorm.bias, 1e-12)
+            at = self.hf.encoder.layer[0].attention
+            q = F.linear(x, at.self.query.weight, at.self.query.bias)
+            k = F.linear(x, at.self.key.weight, at.self.key.bias)
+            v = F.linear(x, at.self.value.weight, at.self.value.bias)
+            ctx = zoo.self_attention(q, k, v, 12)
+            return zoo.add_layer_norm(ctx, x, at.output.LayerNorm.weight, at.output.LayerNorm.bias, 1e-12)
+
+    torch.manual_seed(0)
+    cfg = BertConfig(num_hidden_layers=1)
+    hf = BertModel(cfg).eval()
+    m = OneLayer(hf).eval()
+    ids = torch.randint(0, cfg.vocab_size, (1, 128))
+    sg = engine.compile(m, ids, device=0, profile_reps=2, dtype="bf16")
+    y = sg.run(ids.cuda())
+    with torch.no_grad():
+        ref = m.double()(ids)
+    assert _rel(y.float().reshape(ref.shape).cpu(), ref) < 1e-2

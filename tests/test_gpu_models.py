@@ -79,3 +79,18 @@ def test_trace_shows_branch_overlap():
     seq, seq_span = stats(sg.trace(engine.SLOT_SEQUENTIAL))
     assert par > 10 and par > 2 * seq, (par, seq)
     assert par_span < 0.85 * seq_span, (par_span, seq_span)
+
+
+def test_bert_base_bf16_parity():
+    """BERT-base seq 128 bf16 through tcgen05 GEMMs + attention vs HF BertModel
+    (fp32 eager forward): last_hidden_state and pooler_output within 1e-2."""
+    from paper_2312_10351_b200 import engine, zoo
+    model, ref_model, ids = zoo.build_bert()
+    sg = engine.compile(model, ids, device=0, profile_reps=2, dtype="bf16")
+    hidden, pooled = sg.run(ids.cuda())
+    h_seq, p_seq = sg.run(ids.cuda(), slot=engine.SLOT_SEQUENTIAL)
+    assert torch.equal(hidden, h_seq) and torch.equal(pooled, p_seq)
+    with torch.no_grad():
+        ref_h, ref_p = ref_model.cuda()(ids.cuda())
+    assert _rel(hidden.float().reshape(ref_h.shape), ref_h) < 1e-2
+    assert _rel(pooled.float().reshape(ref_p.shape), ref_p) < 1e-2
