@@ -70,7 +70,7 @@ def conv_engine_for(op, requested: int) -> int:
     the exact-fp32 SIMT kernel."""
     if op.kind != CONV2D:
         return requested
-    if op.output.dtype == "bf16":
+    if op.output.dtype == "bf16" or op.inputs[0].root()[0].dtype == "bf16":
         return 2
     if requested != 1:
         return requested

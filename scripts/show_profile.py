@@ -1,6 +1,6 @@
 import json, sys
 name = sys.argv[1]
-d = json.load(open(f"gpurun_out/profile_{name}.json"))
+d = json.load(open(f"gpurun_out/profile_{name}.json"))  # name = MODEL_DTYPE[_bounded]
 ops = d["ops"]
 print(name, "sum isolated", round(sum(o["isolated_us"] for o in ops), 1), "cp", round(d["critical_path_us"], 1))
 n = len(ops); preds = {i + 1: [] for i in range(n)}
