@@ -148,6 +148,26 @@ def cpu_reference(graph_dict: dict, cfg: dict, budget_s: float, procs: int) -> d
 # ----------------------------------------------------------------- GPU arm
 
 
+def build_workload(args):
+    """(model, reference model, example input(s)) of the configured workload."""
+    from paper_2312_10351_b200 import zoo
+    if args.model == "bert_base":
+        model, ref_model, x = zoo.build_bert()
+        args.dtype = "bf16"  # BASELINE config: BERT-base seq 128 bf16
+        return model, ref_model, x
+    if args.model == "deepfm":
+        model, x = zoo.build_deepfm(args.batch)
+        args.dtype = "f32"   # fp32 recommendation model (the MLP runs on the exact-fp32 engine)
+        return model, model, x
+    model, x = zoo.build(args.model, batch=args.batch)
+    return model, model, x
+
+
+def workload_name(args, x) -> str:
+    shape = "+".join("x".join(map(str, t.shape)) for t in (x if isinstance(x, tuple) else (x,)))
+    return f"{args.model} batch={args.batch} {args.dtype} ({shape})"
+
+
 def run_gpu(args) -> dict | None:
     import torch
     import torch.distributed as dist
@@ -162,20 +182,15 @@ def run_gpu(args) -> dict | None:
     from paper_2312_10351_b200 import engine, zoo
     from paper_2312_10351_b200.dag import graph_to_dict
 
-    if args.model == "bert_base":
-        model, ref_model, x = zoo.build_bert()
-        args.dtype = "bf16"  # BASELINE config: BERT-base seq 128 bf16
-    else:
-        model, x = zoo.build(args.model)
-        ref_model = model
+    model, ref_model, x = build_workload(args)
     sg = engine.compile(model, x, device=local, bound_grids=args.bounded, profile_reps=args.profile_reps,
                         dtype=args.dtype)
-    xd = x.cuda(local)
+    xd = tuple(t.cuda(local) for t in x) if isinstance(x, tuple) else x.cuda(local)
     # correctness guard on every rank: a fast wrong answer is not a result
     y = sg.run(xd)
     y = y[0] if isinstance(y, tuple) else y
     with torch.no_grad():
-        ref = ref_model.cuda(local)(xd)
+        ref = ref_model.cuda(local)(*xd) if isinstance(xd, tuple) else ref_model.cuda(local)(xd)
     ref = ref[0] if isinstance(ref, tuple) else ref
     y = y.float().reshape(ref.shape)
     rel = (torch.linalg.vector_norm(y - ref) / torch.linalg.vector_norm(ref)).item()
@@ -202,7 +217,7 @@ def run_gpu(args) -> dict | None:
     e2e = sg.time_host_roundtrip(x, warmup=args.warmup, iters=args.steps)
 
     if world > 1:
-        tt = torch.tensor([step_total_s, e2e["seconds"]], dtype=torch.float64, device=xd.device)
+        tt = torch.tensor([step_total_s, e2e["seconds"]], dtype=torch.float64, device=torch.device("cuda", local))
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         step_total_s, e2e_s = tt.tolist()
     else:
@@ -230,8 +245,9 @@ def run_gpu(args) -> dict | None:
             name = {0: "conv2d_f32_simt", 1: "conv2d_tc_tf32x3", 2: "conv2d_tc_bf16"}[
                 engine.conv_engine_for(op, sg.conv_engine)]
         else:
-            name = {2: "maxpool2d", 3: "avgpool2d", 4: "global_avgpool", 5: "linear_f32", 7: "layernorm",
-                    9: "embedding", 10: "attention_tc"}[op.kind]
+            name = {2: "maxpool2d", 3: "avgpool2d", 4: "global_avgpool", 5: "linear_f32", 6: "add",
+                    7: "layernorm", 9: "embedding", 10: "attention_tc", 11: "copy", 12: "fm", 13: "dwconv2d",
+                    14: "relu", 16: "field_embedding", 17: "first_order"}[op.kind]
         f = fam.setdefault(name, {"us": 0.0, "flops": 0, "bytes": 0, "launches": 0})
         f["us"] += p["isolated_us"]
         f["flops"] += op.flops
@@ -296,7 +312,7 @@ def run_gpu(args) -> dict | None:
     cpu = cpu_reference(gd, gcfg, args.cpu_seconds, 1)
 
     launches = sg.num_launches(engine.SLOT_PARALLEL)
-    value = world * args.steps / step_total_s
+    value = world * args.batch * args.steps / step_total_s
     line = {
         "metric": "batch-1 inference throughput (inferences/s); batch-1 latency ms and speed-up vs the "
                   "sequential single-stream CUDA Graph of the same kernels reported beside it",
@@ -311,7 +327,7 @@ def run_gpu(args) -> dict | None:
         "vs_baseline": None,
         "dtype": args.dtype,
         "data": "synthetic input, random-init weights (seed 0), BN stats randomised",
-        "config": {"workload": f"{args.model} batch=1 {args.dtype} ({'x'.join(map(str, x.shape))} NCHW)",
+        "config": {"workload": workload_name(args, x),
                    "parallelism": f"{world} independent replica(s), no collective",
                    "l2": "flushed (256 MiB memset) before every timed step, outside the event bracket",
                    "dag_nodes": len(sg.graph), "dag_edges": len(sg.graph.edges),
@@ -332,14 +348,14 @@ def run_gpu(args) -> dict | None:
         "roofline": roofline,
         "rel_err_vs_torch_fp32": rel,
         "rel_tolerance": 1e-4 if args.dtype == "f32" else 1e-2,
-        "e2e": {"value": round(world * args.steps / e2e_s, 2), "unit": "inferences/s",
+        "e2e": {"value": round(world * args.batch * args.steps / e2e_s, 2), "unit": "inferences/s",
                 "h2d_bytes_per_step": e2e["h2d_bytes"], "d2h_bytes_per_step": e2e["d2h_bytes"],
-                "path": "ScheduledGraph.run_host: pinned host NCHW input -> H2D -> graph replay -> "
-                        "D2H logits, per step, CUDA events around all three"},
+                "path": "ScheduledGraph.run_host: pinned host input(s) -> H2D -> graph replay -> "
+                        "D2H of the output, per step, CUDA events around all three"},
         "gpu_launches": launches * args.steps,
         "gpu_launches_per_step": launches,
         "clocks": clk.summary(),
-        "cpu_baseline": {"value": round(cpu["value"], 3), "unit": "inferences/s", "cores": 1,
+        "cpu_baseline": {"value": round(cpu["value"] * args.batch, 3), "unit": "inferences/s", "cores": 1,
                          "kind": "port",
                          "sample": f"{cpu['runs']} runs of oracle allocate_streams + order_opara + "
                                    f"simulate (the reference's 'run') on the profiled {args.model} DAG, "
@@ -356,11 +372,11 @@ def run_reference(args) -> dict | None:
     world, rank, _ = _dist()
     if rank != 0:
         return None
-    from paper_2312_10351_b200 import frontend, zoo
+    from paper_2312_10351_b200 import frontend
     from paper_2312_10351_b200.dag import graph_to_dict
     import paper_2312_10351_b200.engine as engine
-    model, x = zoo.build(args.model)
-    prog = frontend.lower(model, x)
+    model, _, x = build_workload(args)
+    prog = frontend.lower(model, x, args.dtype)
     g = engine.static_dag(prog)  # same topology / classes; launch-config demands
     gd = graph_to_dict(g)
     cfg = {"num_sms": 148, "threads_per_sm": 2048, "shared_mem_per_sm": 233472,
@@ -377,7 +393,7 @@ def run_reference(args) -> dict | None:
         vals.append(r["value"])
         runs += r["runs"]
     el = time.perf_counter() - t0
-    v = statistics.median(vals)
+    v = statistics.median(vals) * args.batch   # one simulated DAG run serves `batch` requests
     return {
         "impl": "reference",
         "metric": "batch-1 inference throughput (inferences/s); batch-1 latency ms and speed-up vs the "
@@ -386,8 +402,8 @@ def run_reference(args) -> dict | None:
         "warmup": args.warmup, "ms_per_step": round(1e3 / v, 3) if v else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic DAG of the model (launch-config demands)",
-        "config": {"workload": f"{args.model} batch=1 DAG: reference CPU path (allocate_streams + "
-                               f"order_opara + simulate)", "processes": cores},
+        "config": {"workload": workload_name(args, x), "path": "reference CPU path (allocate_streams + "
+                               "order_opara + simulate) on the model's DAG", "processes": cores},
         "cpu_baseline": {"value": round(v, 3), "unit": "inferences/s", "cores": cores, "kind": "port",
                          "sample": f"{runs} simulated runs in {el:.1f} s across {cores} processes"},
         "e2e": {"value": round(v, 3), "unit": "inferences/s", "h2d_bytes_per_step": 0,
@@ -401,7 +417,9 @@ def main(argv=None) -> int:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--model", default="inception_v3", choices=["inception_v3", "googlenet", "bert_base"])
+    ap.add_argument("--model", default="inception_v3",
+                    choices=["inception_v3", "googlenet", "bert_base", "nasnet_large", "deepfm"])
+    ap.add_argument("--batch", type=int, default=1, help="requests per inference (DeepFM batch sweep 1-32)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])

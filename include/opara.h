@@ -148,16 +148,18 @@ typedef enum opara_op_kind {
   OPARA_OP_AVGPOOL2D = 3,   /* NHWC window mean (count_include_pad aware)                 */
   OPARA_OP_GLOBAL_AVGPOOL = 4,
   OPARA_OP_LINEAR = 5,      /* y = act(x W^T + b), row-major                              */
-  OPARA_OP_ADD = 6,         /* y = a + b (+ReLU)                                          */
+  OPARA_OP_ADD = 6,         /* y = act(x0 + .. + x3) over channel views (csrc/elementwise.cu) */
   OPARA_OP_LAYERNORM = 7,   /* y = LN(x (+ residual))                                     */
   OPARA_OP_GELU = 8,
   OPARA_OP_EMBEDDING = 9,   /* row gather (+ position + type rows)                        */
   OPARA_OP_ATTENTION = 10,  /* softmax(Q K^T * scale + mask) V per head                   */
-  OPARA_OP_COPY = 11,       /* strided channel-slice copy                                 */
-  OPARA_OP_FM = 12,         /* factorization-machine interaction                          */
-  OPARA_OP_DWCONV2D = 13,   /* depthwise conv                                             */
-  OPARA_OP_RELU = 14,
-  OPARA_OP_SOFTMAX = 15
+  OPARA_OP_COPY = 11,       /* strided channel-slice copy (+act)                          */
+  OPARA_OP_FM = 12,         /* factorization-machine interaction      (csrc/deepfm.cu)    */
+  OPARA_OP_DWCONV2D = 13,   /* depthwise conv, fused input ReLU       (csrc/dwconv.cu)    */
+  OPARA_OP_RELU = 14,       /* unfused ReLU over a channel view                           */
+  OPARA_OP_SOFTMAX = 15,    /* reserved                                                   */
+  OPARA_OP_FIELD_EMBEDDING = 16, /* per-field embedding row gather into a slice (deepfm.cu) */
+  OPARA_OP_FIRST_ORDER = 17 /* DeepFM linear part: sum of per-field weights + dense dot    */
 } opara_op_kind;
 
 #define OPARA_OP_MAX_INTS 40

@@ -28,7 +28,7 @@ struct ConvArgs {
   int N, H, W, Cin, in_cs, in_coff;
   int OH, OW, Cout, out_cs, out_coff;
   int R, S, sh, sw, ph, pw;
-  int relu;
+  int relu, relu_in;
   int M, K;
   int splits, kt_per_split;
   // input element (b, ih, iw, c) lives at in[b*sN + ih*sH + iw*sW + c*sC + in_coff]
@@ -103,6 +103,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
         ra[j][0] = v.x; ra[j][1] = v.y; ra[j][2] = v.z; ra[j][3] = v.w;
       } else {
         ra[j][0] = ok ? __ldg(src) : 0.f;
+      }
+      if (a.relu_in) {  // fused input ReLU
+#pragma unroll
+        for (int e = 0; e < AV; ++e) ra[j][e] = fmaxf(ra[j][e], 0.f);
       }
     }
 #pragma unroll
@@ -282,6 +286,7 @@ opara_status launch_conv2d(const opara_op& op, cudaStream_t s, unsigned long lon
   a.out_cs = (int)op.i[9]; a.out_coff = (int)op.i[10];
   a.R = (int)op.i[11]; a.S = (int)op.i[12]; a.sh = (int)op.i[13]; a.sw = (int)op.i[14];
   a.ph = (int)op.i[15]; a.pw = (int)op.i[16]; a.relu = (int)op.i[17];
+  a.relu_in = (int)op.i[25];
   if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "conv2d simt engine: fp32 only");
   a.M = a.N * a.OH * a.OW;
   a.K = a.R * a.S * a.Cin;

@@ -60,7 +60,7 @@ struct TcArgs {
   int N, H, W, Cin, in_coff;
   int OH, OW, Cout, out_cs, out_coff;
   int R, S, sh, sw, ph, pw;
-  int relu, vec_out;
+  int relu, vec_out, relu_in;
   int M, K, kblocks;
   int splits, kb_per_split;
   int64_t sN, sH, sW, sC;
@@ -244,7 +244,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
           // The tensor core reads an fp32 operand as tf32 by dropping the low
           // 13 mantissa bits, so the raw x already serves as the hi plane;
           // only lo = x - trunc_tf32(x) (exact in fp32) is materialised.
-          const float4 v = *reinterpret_cast<const float4*>(xh + x_off(j));
+          float4 v = *reinterpret_cast<const float4*>(xh + x_off(j));
+          if (a.relu_in) {  // fused input ReLU: clamp the hi plane in place
+            v.x = fmaxf(v.x, 0.f);
+            v.y = fmaxf(v.y, 0.f);
+            v.z = fmaxf(v.z, 0.f);
+            v.w = fmaxf(v.w, 0.f);
+            *reinterpret_cast<float4*>(xh + x_off(j)) = v;
+          }
           float4 lo;
           lo.x = v.x - tc::trunc_tf32(v.x);
           lo.y = v.y - tc::trunc_tf32(v.y);
@@ -515,6 +522,7 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   a.out_cs = (int)op.i[9]; a.out_coff = (int)op.i[10];
   a.R = (int)op.i[11]; a.S = (int)op.i[12]; a.sh = (int)op.i[13]; a.sw = (int)op.i[14];
   a.ph = (int)op.i[15]; a.pw = (int)op.i[16]; a.relu = (int)op.i[17];
+  a.relu_in = (int)op.i[25];
   if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "conv2d tc engine: fp32 (3xTF32) only");
   a.M = a.N * a.OH * a.OW;
   a.K = a.R * a.S * a.Cin;

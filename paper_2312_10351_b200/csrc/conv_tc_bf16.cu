@@ -50,7 +50,7 @@ struct BfArgs {
   int N, H, W, Cin, in_coff;
   int OH, OW, Cout, out_cs, out_coff;
   int R, S, sh, sw, ph, pw;
-  int act, vec_out;
+  int act, vec_out, relu_in;
   int M, K, kblocks;
   int splits, kb_per_split;
   int64_t sN, sH, sW, sC;
@@ -59,6 +59,10 @@ struct BfArgs {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ float act_fn(float v, int act) {
   if (act == 1) return fmaxf(v, 0.f);
@@ -145,6 +149,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
         dr = rs / a.S;
         dq = rs - dr * a.S;
       }
+      // Fused input ReLU (relu_in): the copies of stage i are committed as one
+      // cp.async group; once stage i-1's group has landed this thread clamps
+      // its own chunks of it in place (bf16 max with 0), fences them into the
+      // async proxy and arrives, so the transform trails the gather by a stage.
+      auto relu_stage = [&](int st) {
+        uint8_t* xs_g = smem + st * kStage + kWBytes;
+#pragma unroll
+        for (int j = 0; j < kRowsPerThread; ++j) {
+          if (rw + 4 * j >= kRowGroups) break;
+          uint4* q = reinterpret_cast<uint4*>(xs_g + x_off(j));
+          uint4 v = *q;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+          const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) h[e] = __hmax2(h[e], z);
+          *q = v;
+        }
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&full[st]);
+      };
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
@@ -157,7 +181,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
           const bool ok = kin && pb[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
           if (rw + 4 * j < kRowGroups) cp_async16(xs + x_off(j), ok ? rowbase[j] + koff : in, ok);
         }
-        tc::cp_async_arrive_noinc(&full[s]);
+        if (a.relu_in) {
+          cp_async_commit();
+          if (i > 0) {
+            cp_async_wait<1>();
+            relu_stage((i - 1) % kStages);
+          }
+        } else {
+          tc::cp_async_arrive_noinc(&full[s]);
+        }
         kc += kBK;
         dc += kBK;
         while (dc >= a.Cin) {
@@ -167,6 +199,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
             ++dr;
           }
         }
+      }
+      if (a.relu_in && nkb > 0) {
+        cp_async_wait<0>();
+        relu_stage((nkb - 1) % kStages);
       }
     } else {
       using TIn = typename std::conditional<kMode == kScalarF32, float, __nv_bfloat16>::type;
@@ -196,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
             if (ok) {
               const TIn t = in[pb[j] * a.sN + ih * a.sH + iw * a.sW + c * a.sC + a.in_coff];
               if constexpr (kMode == kScalarF32) x = t; else x = __bfloat162float(t);
+              if (a.relu_in) x = fmaxf(x, 0.f);
             }
             v[j][e] = __float2bfloat16_rn(x);
           }
@@ -396,8 +433,8 @@ int64_t max_clusters(const void* func, int size, size_t smem) {
 }  // namespace
 
 // CONV2D with i[22] == 2 (engine "tc_bf16"): i[18] = input dtype (0 f32, 1 bf16),
-// i[23] = output dtype, i[24] = activation (0 none, 1 ReLU, 2 GELU; i[17]
-// relu=1 also selects ReLU); p[1] = bf16 weights packed by
+// i[23] = output dtype, i[24] = activation (0 none, 1 ReLU, 2 GELU, 3 tanh;
+// i[17] relu=1 also selects ReLU), i[25] = relu_in; p[1] = bf16 weights packed by
 // engine.pack_conv_weights_bf16.
 opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned long long* trace,
                                    LaunchCfg* cfg, bool dry) {
@@ -414,6 +451,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   a.R = (int)op.i[11]; a.S = (int)op.i[12]; a.sh = (int)op.i[13]; a.sw = (int)op.i[14];
   a.ph = (int)op.i[15]; a.pw = (int)op.i[16];
   a.act = op.i[24] ? (int)op.i[24] : (op.i[17] ? 1 : 0);
+  a.relu_in = (int)op.i[25];
   const bool in_f32 = op.i[18] == 0;
   const bool out_f32 = op.i[23] == 0;
   a.M = a.N * a.OH * a.OW;

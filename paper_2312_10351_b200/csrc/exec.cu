@@ -79,6 +79,13 @@ opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* t
     case OPARA_OP_LAYERNORM:
     case OPARA_OP_EMBEDDING: return launch_rows(op, s, trace, cfg, dry);
     case OPARA_OP_ATTENTION: return launch_attention(op, s, trace, cfg, dry);
+    case OPARA_OP_ADD:
+    case OPARA_OP_COPY:
+    case OPARA_OP_RELU: return launch_elementwise(op, s, trace, cfg, dry);
+    case OPARA_OP_DWCONV2D: return launch_dwconv2d(op, s, trace, cfg, dry);
+    case OPARA_OP_FIELD_EMBEDDING:
+    case OPARA_OP_FIRST_ORDER:
+    case OPARA_OP_FM: return launch_deepfm(op, s, trace, cfg, dry);
     default: return fail(OPARA_ERR_VALUE, "unsupported op kind " + std::to_string(op.kind));
   }
 }

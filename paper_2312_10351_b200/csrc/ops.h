@@ -11,7 +11,8 @@
 //                 17 relu, 18 dtype (0 f32), 19 split_k (1),
 //                 20 in_nchw (1: input is a dense NCHW tensor, e.g. the graph input),
 //                 21 target CTAs for split-K (0 = default), 22 engine (0 SIMT fp32,
-//                 1 tcgen05 3xTF32)
+//                 1 tcgen05 3xTF32, 2 tcgen05 bf16), 23 output dtype, 24 activation
+//                 (0 none, 1 ReLU, 2 GELU, 3 tanh), 25 relu_in (ReLU fused on the input)
 //              p: 0 in, 1 weight: engine 0 [R*S*Cin][Cout] (k = (r*S + s)*Cin + c);
 //                 engine 1 packed tf32 hi/lo UMMA images (conv_tc.cu), 2 bias [Cout], 3 out,
 //                 7 split-K workspace (executor-owned)
@@ -20,7 +21,10 @@
 // AVGPOOL2D       9 out_coff, 10 kh, 11 kw, 12 sh, 13 sw, 14 ph, 15 pw,
 //                 16 count_include_pad (avg), 18 dtype
 //              p: 0 in, 3 out
-// GLOBAL_AVGPOOL i: 0 N, 1 H, 2 W, 3 C, 4 in_cstride, 5 in_coff, 18 dtype;  p: 0 in, 3 out [N][C]
+// GLOBAL_AVGPOOL i: 0 N, 1 H, 2 W, 3 C, 4 in_cstride, 5 in_coff, 8 out_cstride (0 = C),
+//                 17 relu_in, 18 dtype;  p: 0 in, 3 out fp32 (first channel of the output view)
+// ADD / COPY / RELU, DWCONV2D, FIELD_EMBEDDING / FIRST_ORDER / FM: see the header comment of
+//              elementwise.cu, dwconv.cu and deepfm.cu
 // LINEAR       i: 0 M (rows), 1 K, 2 N (out features), 3 act (0 none, 1 relu, 2 gelu, 3 tanh),
 //                 4 x_stride, 5 y_stride, 18 dtype
 //              p: 0 x [M][K], 1 W [N][K], 2 bias [N] (nullable), 3 y [M][N]
@@ -65,6 +69,9 @@ opara_status launch_global_avgpool(const opara_op&, cudaStream_t, unsigned long 
 opara_status launch_linear(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
 opara_status launch_rows(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
 opara_status launch_attention(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+opara_status launch_elementwise(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+opara_status launch_dwconv2d(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
+opara_status launch_deepfm(const opara_op&, cudaStream_t, unsigned long long*, LaunchCfg*, bool);
 
 // Dispatch on op.kind.
 opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* trace,

@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long lon
 template <typename T>
 __global__ void __launch_bounds__(256) global_avgpool_nhwc(const T* __restrict__ in,
                                                            float* __restrict__ out, int N, int HW,
-                                                           int C, int in_cs, int in_coff,
-                                                           unsigned long long* trace) {
+                                                           int C, int in_cs, int in_coff, int relu_in,
+                                                           int out_cs, unsigned long long* trace) {
   pdl_trigger();
   pdl_wait();
   trace_begin(trace);  // timeline starts once the inputs are ready (after the PDL wait)
@@ -121,10 +121,12 @@ __global__ void __launch_bounds__(256) global_avgpool_nhwc(const T* __restrict__
     const int c = static_cast<int>(w % C);
     const int b = static_cast<int>(w / C);
     float s = 0.f;
-    for (int p = lane; p < HW; p += 32)
-      s += to_f(in[(static_cast<int64_t>(b) * HW + p) * in_cs + in_coff + c]);
+    for (int p = lane; p < HW; p += 32) {
+      const float v = to_f(in[(static_cast<int64_t>(b) * HW + p) * in_cs + in_coff + c]);
+      s += relu_in ? fmaxf(v, 0.f) : v;
+    }
     s = warp_sum(s);
-    if (lane == 0) out[static_cast<int64_t>(b) * C + c] = s / static_cast<float>(HW);
+    if (lane == 0) out[static_cast<int64_t>(b) * out_cs + c] = s / static_cast<float>(HW);
   }
   trace_end(trace);
 }
@@ -135,7 +137,7 @@ template <typename T>
 __global__ void __launch_bounds__(128) global_avgpool_nhwc_cols(const T* __restrict__ in,
                                                                 float* __restrict__ out, int N,
                                                                 int HW, int C, int in_cs,
-                                                                int in_coff,
+                                                                int in_coff, int relu_in, int out_cs,
                                                                 unsigned long long* trace) {
   pdl_trigger();
   pdl_wait();
@@ -147,8 +149,11 @@ __global__ void __launch_bounds__(128) global_avgpool_nhwc_cols(const T* __restr
     const int b = static_cast<int>(t / C);
     const T* src = in + static_cast<int64_t>(b) * HW * in_cs + in_coff + c;
     float s = 0.f;
-    for (int p = 0; p < HW; ++p) s += to_f(src[static_cast<int64_t>(p) * in_cs]);
-    out[t] = s / static_cast<float>(HW);
+    for (int p = 0; p < HW; ++p) {
+      const float v = to_f(src[static_cast<int64_t>(p) * in_cs]);
+      s += relu_in ? fmaxf(v, 0.f) : v;
+    }
+    out[static_cast<int64_t>(b) * out_cs + c] = s / static_cast<float>(HW);
   }
   trace_end(trace);
 }
@@ -197,7 +202,8 @@ opara_status launch_global_avgpool(const opara_op& op, cudaStream_t s, unsigned 
   const void* in = op.p[0];
   float* out = static_cast<float*>(op.p[3]);  // always fp32 (feeds the classifier)
   int N = (int)op.i[0], H = (int)op.i[1], W = (int)op.i[2], C = (int)op.i[3];
-  int in_cs = (int)op.i[4], in_coff = (int)op.i[5];
+  int in_cs = (int)op.i[4], in_coff = (int)op.i[5], relu_in = (int)op.i[17];
+  int out_cs = op.i[8] > 0 ? (int)op.i[8] : C;   // p[3] points at the output view's first channel
   const bool bf = op.i[18] == 1;
   int HW = H * W;
   LaunchCfg c;
@@ -215,7 +221,7 @@ opara_status launch_global_avgpool(const opara_op& op, cudaStream_t s, unsigned 
   }
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
-  void* args[] = {&in, &out, &N, &HW, &C, &in_cs, &in_coff, &trace};
+  void* args[] = {&in, &out, &N, &HW, &C, &in_cs, &in_coff, &relu_in, &out_cs, &trace};
   return launch_kernel(c, args, s);
 }
 

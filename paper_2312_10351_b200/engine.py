@@ -31,10 +31,13 @@ import torch
 from . import _lib
 from .dag import ComputationGraph, OperatorNode, ResourceDemand, graph_to_dict
 from .device import GpuConfig, device_gpu_config, GPU_PRESETS
-from .frontend import (ATTENTION, AVGPOOL2D, CONV2D, EMBEDDING, GLOBAL_AVGPOOL, LAYERNORM, LINEAR, MAXPOOL2D,
-                       NOP, Program, lower)
+from .frontend import (ADD, ATTENTION, AVGPOOL2D, CONV2D, COPY, DWCONV2D, EMBEDDING, FIELD_EMBEDDING, FIRST_ORDER,
+                       FM, GLOBAL_AVGPOOL, LAYERNORM, LINEAR, MAXPOOL2D, NOP, RELU, Program, lower)
 from .order import LaunchSchedule, make_order
 from .plan import StreamPlan, allocate_streams, plan_to_dict, single_stream_plan
+
+# kinds whose records are built from every input view + named host arrays
+ROW_KINDS = (LAYERNORM, EMBEDDING, ATTENTION, ADD, COPY, RELU, FIELD_EMBEDDING, FIRST_ORDER, FM)
 
 SLOT_PARALLEL = 0
 SLOT_SEQUENTIAL = 1
@@ -165,7 +168,7 @@ def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -
     rec.variant = -1
     if op.kind == NOP:
         return rec
-    if op.kind in (LAYERNORM, EMBEDDING, ATTENTION):
+    if op.kind in ROW_KINDS:
         return _row_record(rec, op, views, weights)
     q = op.ints
     (ib, icoff, ics, inchw), (ob, ocoff, ocs) = views
@@ -175,7 +178,11 @@ def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -
         vals = [q["N"], q["H"], q["W"], q["Cin"], ics, icoff, q["OH"], q["OW"], q["Cout"], ocs, ocoff,
                 q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], in_dt if conv_engine == 2 else 0,
                 1, int(inchw), int(target_ctas), conv_engine, DTYPE_CODE[op.output.dtype],
-                q.get("act", 1 if q["relu"] else 0)]
+                q.get("act", 1 if q["relu"] else 0), q.get("relu_in", 0)]
+        rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
+    elif op.kind == DWCONV2D:
+        vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff, q["OH"], q["OW"], ocs, ocoff, q["kh"], q["kw"],
+                q["sh"], q["sw"], q["ph"], q["pw"], q["relu_in"], q["act"], DTYPE_CODE[op.output.dtype]]
         rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
     elif op.kind in (MAXPOOL2D, AVGPOOL2D):
         vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff, q["OH"], q["OW"], ocs, ocoff, q["kh"],
@@ -183,11 +190,12 @@ def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -
                 DTYPE_CODE[op.inputs[0].root()[0].dtype]]
         rec.p[0], rec.p[3] = ib, ob
     elif op.kind == GLOBAL_AVGPOOL:
-        vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff] + [0] * 12 + [DTYPE_CODE[op.inputs[0].root()[0].dtype]]
-        rec.p[0], rec.p[3] = ib, ob
+        vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff, 0, 0, ocs] + [0] * 8 + [
+            q.get("relu_in", 0), DTYPE_CODE[op.inputs[0].root()[0].dtype]]
+        rec.p[0], rec.p[3] = ib, _at(ob, ocoff, 4)
     elif op.kind == LINEAR:
-        vals = [q["M"], q["K"], q["N"], q["act"], q["K"], q["N"]] + [0] * 12 + [0]
-        rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
+        vals = [q["M"], q["K"], q["N"], q["act"], ics, ocs] + [0] * 12 + [0]
+        rec.p[0], rec.p[1], rec.p[2], rec.p[3] = _at(ib, icoff, 4), weights[0], weights[1], _at(ob, ocoff, 4)
     else:
         raise ValueError(f"unknown op kind {op.kind}")
     for k, v in enumerate(vals):
@@ -195,14 +203,42 @@ def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -
     return rec
 
 
+def _at(ptr, elems, esize):
+    """Device address `elems` elements past `ptr` (None stays None)."""
+    return None if ptr is None else ptr + esize * elems
+
+
 def _row_record(rec, op, views, arrays):
-    """Records of the transformer row kernels (layouts: csrc/norm.cu, attention_tc.cu).
-    `views` = [(ptr, coff, cstride, ...)] for the inputs then the output;
-    `arrays` = device pointers of op.arrays by name."""
+    """Records of the row / elementwise / DeepFM kernels (layouts: csrc/norm.cu,
+    attention_tc.cu, elementwise.cu, deepfm.cu).  `views` = [(ptr, coff,
+    cstride, ...)] for the inputs then the output; `arrays` = device pointers
+    of op.arrays by name."""
     q = op.ints
     *ins, (ob, ocoff, ocs) = views
     esize = 2 if op.output.dtype == "bf16" else 4
-    if op.kind == EMBEDDING:
+    if op.kind in (ADD, COPY, RELU):
+        n = len(ins)
+        vals = [q["P"], q["C"], n, q.get("act", 0), ocs, ocoff] + [0] * 8
+        slots = (0, 1, 2, 4)
+        for j, (ib, icoff, ics, _) in enumerate(ins):
+            vals[6 + j], vals[10 + j] = ics, icoff
+            rec.p[slots[j]] = ib
+        vals += [0] * 4 + [DTYPE_CODE[op.output.dtype]]
+        rec.p[3] = ob
+    elif op.kind == FIELD_EMBEDDING:
+        (ib, icoff, ics, _), = ins
+        vals = [q["B"], q["dim"], q["field"] + icoff, ics, ocs, ocoff, q["vocab"]]
+        rec.p[0], rec.p[1], rec.p[3] = ib, arrays["table"], ob
+    elif op.kind == FIRST_ORDER:
+        (ib, icoff, ics, _), (db, dcoff, dcs, _) = ins
+        vals = [q["B"], q["fields"], ics, q["n_dense"], dcs, q["vocab"], ocs]
+        rec.p[0], rec.p[1], rec.p[2] = _at(ib, icoff, 8), arrays["w1"], arrays["wd"]
+        rec.p[4], rec.p[3] = _at(db, dcoff, 4), _at(ob, ocoff, 4)
+    elif op.kind == FM:
+        (ib, icoff, ics, _), = ins
+        vals = [q["B"], q["fields"], q["dim"], ics, icoff, ocs]
+        rec.p[0], rec.p[3] = ib, _at(ob, ocoff, 4)
+    elif op.kind == EMBEDDING:
         vals = [q["rows"], q["C"], 0, 0, ocs, 0]
         rec.p[0], rec.p[1] = ins[0][0], None
         rec.p[2], rec.p[3], rec.p[4] = arrays["gamma"], arrays["beta"], ob + esize * ocoff
@@ -249,7 +285,7 @@ class ScheduledGraph:
         recs = (_lib.OparaOp * len(program.ops))()
         self.targets = concurrency_targets(program) if bound_grids else {}
         for k, op in enumerate(program.ops):
-            if op.kind in (LAYERNORM, EMBEDDING, ATTENTION):
+            if op.kind in ROW_KINDS:
                 recs[k] = _op_record(op, self._all_views(op), self._arrays(op))
             else:
                 recs[k] = _op_record(op, self._views(op), self._weights(op),
@@ -289,8 +325,8 @@ class ScheduledGraph:
             else:
                 buf = torch.zeros(t.shape, dtype=tdt, device=self.dev)
             self._bufs[t.tid] = buf
-        root, _ = program.input.root()
-        self.input_buffer = self._bufs[root.tid]
+        self.input_buffers = [self._bufs[t.root()[0].tid] for t in (program.inputs or [program.input])]
+        self.input_buffer = self.input_buffers[0]
         self.output_buffers = []
         for out in (program.outputs or [program.output]):
             oroot, ooff = out.root()
@@ -378,25 +414,35 @@ class ScheduledGraph:
         s = stream or torch.cuda.current_stream(self.dev)
         _lib.check(_lib.lib().opara_exec_replay(self._h, slot, C.c_void_p(s.cuda_stream)))
 
-    def run(self, x: torch.Tensor, slot: int = SLOT_PARALLEL):
-        """One inference: copy `x` in (NCHW image or [1, T] token ids), replay,
-        return a copy of the output (a tuple when the model has several)."""
-        self.input_buffer.copy_(x.reshape(self.input_buffer.shape), non_blocking=True)
+    def _inputs(self, x) -> list:
+        xs = list(x) if isinstance(x, (tuple, list)) else [x]
+        if len(xs) != len(self.input_buffers):
+            raise ValueError(f"graph takes {len(self.input_buffers)} inputs, got {len(xs)}")
+        return xs
+
+    def run(self, x, slot: int = SLOT_PARALLEL):
+        """One inference: copy the input(s) in (NCHW image, [1, T] token ids,
+        or a tuple such as DeepFM's (dense, ids)), replay, return a copy of the
+        output (a tuple when the model has several)."""
+        for buf, xi in zip(self.input_buffers, self._inputs(x)):
+            buf.copy_(xi.reshape(buf.shape), non_blocking=True)
         self.replay(slot)
         outs = tuple(b.clone() for b in self.output_buffers)
         return outs[0] if len(outs) == 1 else outs
 
-    def run_host(self, x_host: torch.Tensor, out_host: torch.Tensor, slot: int = SLOT_PARALLEL) -> None:
-        """Host-buffer inference (asynchronous): H2D copy of `x_host` (pinned
-        NCHW), replay, D2H copy of the output into `out_host` (pinned)."""
-        self.input_buffer.copy_(x_host, non_blocking=True)
+    def run_host(self, x_host, out_host: torch.Tensor, slot: int = SLOT_PARALLEL) -> None:
+        """Host-buffer inference (asynchronous): H2D copy of the pinned input(s),
+        replay, D2H copy of the first output into `out_host` (pinned)."""
+        for buf, xi in zip(self.input_buffers, self._inputs(x_host)):
+            buf.copy_(xi, non_blocking=True)
         self.replay(slot)
         out_host.copy_(self.output_buffer, non_blocking=True)
 
-    def time_host_roundtrip(self, x: torch.Tensor, warmup: int = 10, iters: int = 100,
+    def time_host_roundtrip(self, x, warmup: int = 10, iters: int = 100,
                             slot: int = SLOT_PARALLEL) -> dict:
         """Time run_host end to end (CUDA events bracketing H2D + replay + D2H)."""
-        x_host = x.detach().to(self.input_buffer.dtype).reshape(self.input_buffer.shape).contiguous().pin_memory()
+        x_host = [xi.detach().to(buf.dtype).reshape(buf.shape).contiguous().pin_memory()
+                  for buf, xi in zip(self.input_buffers, self._inputs(x))]
         out_host = torch.empty(self.output_buffer.shape, dtype=self.output_buffer.dtype).pin_memory()
         s = torch.cuda.current_stream(self.dev)
         for _ in range(warmup):
@@ -411,12 +457,13 @@ class ScheduledGraph:
         s.synchronize()
         ms = [a.elapsed_time(b) for a, b in evs]
         return {"seconds": sum(ms) / 1e3, "median_ms": float(np.median(ms)),
-                "h2d_bytes": x_host.numel() * x_host.element_size(),
+                "h2d_bytes": sum(t.numel() * t.element_size() for t in x_host),
                 "d2h_bytes": out_host.numel() * out_host.element_size()}
 
-    def run_eager(self, x: torch.Tensor, order=None) -> torch.Tensor:
+    def run_eager(self, x, order=None) -> torch.Tensor:
         """Launch every kernel on one stream without a graph (debugging)."""
-        self.input_buffer.copy_(x)
+        for buf, xi in zip(self.input_buffers, self._inputs(x)):
+            buf.copy_(xi.reshape(buf.shape))
         order = self.seq_schedule.order if order is None else order
         arr = np.asarray([v - 1 for v in order], dtype=np.int64)
         s = torch.cuda.current_stream(self.dev)
@@ -512,7 +559,7 @@ def static_dag(program: Program, gpu_config: GpuConfig | None = None,
     targets = concurrency_targets(program) if bound_grids else {}
     nodes = []
     for k, op in enumerate(program.ops):
-        if op.kind in (LAYERNORM, EMBEDDING, ATTENTION):
+        if op.kind in ROW_KINDS:
             views = [(0x1000 * (j + 1), t.root()[1], t.root()[0].shape[-1], False) for j, t in enumerate(op.inputs)]
             views.append((0x9000, op.output.root()[1], op.output.root()[0].shape[-1]))
             rec = _op_record(op, views, {name: 0xA000 for name in op.arrays})

@@ -16,6 +16,7 @@ the scheduler (Alg. 1 / Alg. 2) sees, and the JSON the reference consumes.
 
 from __future__ import annotations
 
+import operator
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -27,8 +28,12 @@ import torch.nn.functional as F
 from .dag import OpClass
 
 # opara_op_kind values (include/opara.h)
-NOP, CONV2D, MAXPOOL2D, AVGPOOL2D, GLOBAL_AVGPOOL, LINEAR = 0, 1, 2, 3, 4, 5
-LAYERNORM, EMBEDDING, ATTENTION = 7, 9, 10
+NOP, CONV2D, MAXPOOL2D, AVGPOOL2D, GLOBAL_AVGPOOL, LINEAR, ADD = 0, 1, 2, 3, 4, 5, 6
+LAYERNORM, EMBEDDING, ATTENTION, COPY, FM, DWCONV2D, RELU = 7, 9, 10, 11, 12, 13, 14
+FIELD_EMBEDDING, FIRST_ORDER = 16, 17
+
+# fused activations (csrc kernels): 0 none, 1 ReLU, 2 GELU (erf), 3 tanh, 4 sigmoid
+ACT_NONE, ACT_RELU, ACT_GELU, ACT_TANH, ACT_SIGMOID = 0, 1, 2, 3, 4
 
 
 @dataclass
@@ -42,6 +47,7 @@ class Tensor:
     alias: "Tensor | None" = None                  # concat parent
     coff_in_alias: int = 0
     nchw_input: bool = False                       # the graph input (dense NCHW)
+    is_graph_input: bool = False
     dtype: str = "f32"                             # "f32" | "bf16" element type of the buffer
 
     def root(self) -> tuple["Tensor", int]:
@@ -73,14 +79,30 @@ class LoweringError(RuntimeError):
     pass
 
 
+_PENDING_ADD = object()   # an add folded into the n-ary ADD of its single add consumer
+
+
+@dataclass
+class Lazy:
+    """A value whose producing transform is folded into its consumers instead
+    of being launched: ReLU (consumers with a fused input ReLU: convs,
+    depthwise convs, global pooling) and/or a stride-2 subsample at offset
+    `sub` (folded into a consuming 1x1 conv as stride 2 and padding -sub)."""
+
+    tensor: Tensor
+    relu: bool = False
+    sub: int | None = None
+
+
 @dataclass
 class Program:
     ops: list
     tensors: list
-    input: Tensor
+    input: Tensor             # first graph input
     output: Tensor            # first graph output
     edges: list               # (u, v) op indices
     outputs: list = field(default_factory=list)
+    inputs: list = field(default_factory=list)
 
 
 def _pool_out(size, k, s, p, ceil_mode):
@@ -116,8 +138,9 @@ class _Lowerer:
         self.esize = 2 if dtype == "bf16" else 4
         self.ops: list[LoweredOp] = []
         self.tensors: list[Tensor] = []
-        self.env: dict[fx.Node, Tensor] = {}
+        self.env: dict = {}
         self.consumed: set[fx.Node] = set()
+        self._materialized: dict[int, Tensor] = {}
 
     def new_tensor(self, shape, producers=(), dtype=None):
         t = Tensor(len(self.tensors), tuple(int(x) for x in shape), set(producers),
@@ -129,6 +152,41 @@ class _Lowerer:
         idx = len(self.ops)
         self.ops.append(op)
         op.output.producers = {idx}
+
+    @staticmethod
+    def _esz(t: Tensor) -> int:
+        return {"bf16": 2, "f32": 4, "i64": 8}[t.dtype]
+
+    # ------------------------------------------------ lazy values (fusion)
+
+    def value(self, arg) -> Tensor:
+        """The materialised tensor of an fx argument: a pending ReLU is
+        launched once as a RELU op (the unfused fallback) and cached."""
+        v = self.env[arg]
+        if not isinstance(v, Lazy):
+            return v
+        if v.sub is not None:
+            raise LoweringError(f"{arg}: a subsample must feed a 1x1 convolution")
+        key = id(v)
+        if key not in self._materialized:
+            t = v.tensor
+            out = self.new_tensor(t.shape, dtype=t.dtype)
+            p, c = self._pixels(t)
+            self.emit(LoweredOp(RELU, "relu", OpClass.MEMORY, dict(P=p, C=c, n=1, act=ACT_RELU), [t], out,
+                                flops=p * c, bytes_min=2 * self._esz(t) * p * c, label=str(arg)))
+            self._materialized[key] = out
+        return self._materialized[key]
+
+    def lazy(self, arg) -> Lazy:
+        v = self.env[arg]
+        return v if isinstance(v, Lazy) else Lazy(v)
+
+    @staticmethod
+    def _pixels(t: Tensor):
+        if len(t.shape) == 4:
+            n, h, w, c = t.shape
+            return n * h * w, c
+        return int(np.prod(t.shape[:-1])), t.shape[-1]
 
     # ----------------------------------------------------------- patterns
 
@@ -148,15 +206,18 @@ class _Lowerer:
             return True
         return n.op == "call_module" and isinstance(self.gm.get_submodule(n.target), nn.ReLU)
 
-    def lower_conv(self, node, conv: nn.Conv2d):
-        if conv.groups != 1 or _pair(conv.dilation) != (1, 1):
-            raise LoweringError(f"{node.name}: grouped/dilated conv not supported by CONV2D")
-        if conv.padding_mode != "zeros" or isinstance(conv.padding, str):
-            raise LoweringError(f"{node.name}: only explicit zero padding is supported")
-        x = self.env[node.args[0]]
+    def _is_sigmoid(self, n):
+        if n.op == "call_function" and n.target in (torch.sigmoid, F.sigmoid):
+            return True
+        return n.op == "call_module" and isinstance(self.gm.get_submodule(n.target), nn.Sigmoid)
+
+    def _is_add(self, n):
+        return n.op == "call_function" and n.target in (operator.add, torch.add) and not n.kwargs
+
+    def _bn_relu_tail(self, node):
+        """conv -> [BatchNorm2d] -> [ReLU] chain starting at `node` (single users only)."""
         bn_node = self._single_user(node, self._is_bn)
-        tail = node
-        bn = None
+        tail, bn = node, None
         if bn_node is not None:
             bn = self.gm.get_submodule(bn_node.target)
             self.consumed.add(bn_node)
@@ -165,22 +226,75 @@ class _Lowerer:
         if relu_node is not None:
             self.consumed.add(relu_node)
             tail = relu_node
+        return tail, bn, relu_node is not None
+
+    def lower_conv(self, node, conv: nn.Conv2d):
+        if _pair(conv.dilation) != (1, 1):
+            raise LoweringError(f"{node.name}: dilated conv not supported")
+        if conv.padding_mode != "zeros" or isinstance(conv.padding, str):
+            raise LoweringError(f"{node.name}: only explicit zero padding is supported")
+        if conv.groups != 1:
+            if conv.groups == conv.in_channels == conv.out_channels:
+                return self.lower_dwconv(node, conv)
+            raise LoweringError(f"{node.name}: grouped conv (other than depthwise) not supported")
+        lz = self.lazy(node.args[0])
+        x = lz.tensor
+        tail, bn, relu = self._bn_relu_tail(node)
         n, h, w, cin = x.shape
         r, s = conv.kernel_size
         sh, sw = _pair(conv.stride)
         ph, pw = _pair(conv.padding)
-        oh = (h + 2 * ph - r) // sh + 1
-        ow = (w + 2 * pw - s) // sw + 1
+        if lz.sub is not None:
+            # subsample(x, off) -> 1x1 conv  ==  1x1 conv with stride 2 reading pixel 2*o + off
+            if (r, s, sh, sw, ph, pw) != (1, 1, 1, 1, 0, 0):
+                raise LoweringError(f"{node.name}: a subsample folds only into a 1x1/s1/p0 conv")
+            sh = sw = 2
+            ph = pw = -lz.sub
+            oh, ow = (h + 1) // 2, (w + 1) // 2   # samples off, off + 2, ... of the zero-extended map
+        else:
+            oh = (h + 2 * ph - r) // sh + 1
+            ow = (w + 2 * pw - s) // sw + 1
         cout = conv.out_channels
         out = self.new_tensor((n, oh, ow, cout))
         wk, b = _fold_bn(conv, bn)
         macs = n * oh * ow * cout * r * s * cin
         op = LoweredOp(CONV2D, "conv", OpClass.COMPUTE,
                        dict(N=n, H=h, W=w, Cin=cin, OH=oh, OW=ow, Cout=cout, R=r, S=s, sh=sh,
-                            sw=sw, ph=ph, pw=pw, relu=int(relu_node is not None)),
+                            sw=sw, ph=ph, pw=pw, relu=int(relu), relu_in=int(lz.relu)),
                        [x], out, wk, b, flops=2 * macs,
-                       bytes_min=(x.dtype == "bf16" and 2 or 4) * n * h * w * cin + self.esize * wk.size
+                       bytes_min=self._esz(x) * n * h * w * cin + self.esize * wk.size
                        + 4 * b.size + self.esize * n * oh * ow * cout,
+                       label=node.name)
+        self.emit(op)
+        self.env[tail] = out
+
+    def lower_dwconv(self, node, conv: nn.Conv2d):
+        lz = self.lazy(node.args[0])
+        if lz.sub is not None:
+            raise LoweringError(f"{node.name}: subsample before a depthwise conv")
+        x = lz.tensor
+        tail, bn, relu = self._bn_relu_tail(node)
+        n, h, w, c = x.shape
+        r, s = conv.kernel_size
+        sh, sw = _pair(conv.stride)
+        ph, pw = _pair(conv.padding)
+        oh = (h + 2 * ph - r) // sh + 1
+        ow = (w + 2 * pw - s) // sw + 1
+        wt = conv.weight.detach().double().cpu()[:, 0]          # [C, r, s]
+        b = conv.bias.detach().double().cpu() if conv.bias is not None else torch.zeros(c, dtype=torch.float64)
+        if bn is not None:
+            scale = bn.weight.detach().double().cpu() / torch.sqrt(bn.running_var.detach().double().cpu() + bn.eps)
+            wt = wt * scale[:, None, None]
+            b = (b - bn.running_mean.detach().double().cpu()) * scale + bn.bias.detach().double().cpu()
+        wk = wt.permute(1, 2, 0).reshape(r * s, c).float().numpy()   # [r*s][C]
+        has_bias = conv.bias is not None or bn is not None
+        out = self.new_tensor((n, oh, ow, c))
+        op = LoweredOp(DWCONV2D, "dwconv", OpClass.MEMORY,
+                       dict(N=n, H=h, W=w, C=c, OH=oh, OW=ow, kh=r, kw=s, sh=sh, sw=sw, ph=ph, pw=pw,
+                            relu_in=int(lz.relu), act=int(relu)),
+                       [x], out, np.ascontiguousarray(wk), b.float().numpy() if has_bias else None,
+                       flops=2 * n * oh * ow * c * r * s,
+                       bytes_min=self._esz(x) * n * h * w * c + 4 * wk.size + self.esize * n * oh * ow * c,
                        label=node.name)
         self.emit(op)
         self.env[tail] = out
@@ -188,11 +302,14 @@ class _Lowerer:
     def lower_pool(self, node, is_max, k, s, p, ceil_mode, include_pad=True, dilation=1):
         if _pair(dilation) != (1, 1):
             raise LoweringError(f"{node.name}: dilated pooling not supported")
-        x = self.env[node.args[0]]
         kh, kw = _pair(k)
         sh, sw = _pair(s if s not in (None, ()) else k)
         ph, pw = _pair(p)
-        n, h, w, c = x.shape
+        lz = self.lazy(node.args[0])
+        n, h, w, c = lz.tensor.shape
+        if not is_max and (kh, kw) == (h, w) and (ph, pw) == (0, 0) and lz.sub is None:
+            return self.lower_gap(node)          # window == whole map: global average pool
+        x = self.value(node.args[0])
         oh = _pool_out(h, kh, sh, ph, ceil_mode)
         ow = _pool_out(w, kw, sw, pw, ceil_mode)
         out = self.new_tensor((n, oh, ow, c))
@@ -205,17 +322,20 @@ class _Lowerer:
         self.env[node] = out
 
     def lower_gap(self, node):
-        x = self.env[node.args[0]]
+        lz = self.lazy(node.args[0])
+        if lz.sub is not None:
+            raise LoweringError(f"{node.name}: subsample before global pooling")
+        x = lz.tensor
         n, h, w, c = x.shape
         out = self.new_tensor((n, c), dtype="f32")  # feeds the fp32 classifier head
-        op = LoweredOp(GLOBAL_AVGPOOL, "pool", OpClass.MEMORY, dict(N=n, H=h, W=w, C=c), [x], out,
-                       flops=n * h * w * c, bytes_min=self.esize * n * h * w * c + 4 * n * c,
+        op = LoweredOp(GLOBAL_AVGPOOL, "pool", OpClass.MEMORY, dict(N=n, H=h, W=w, C=c, relu_in=int(lz.relu)),
+                       [x], out, flops=n * h * w * c, bytes_min=self.esize * n * h * w * c + 4 * n * c,
                        label=node.name)
         self.emit(op)
         self.env[node] = out
 
     def lower_linear(self, node, lin: nn.Linear):
-        x = self.env[node.args[0]]
+        x = self.value(node.args[0])
         if len(x.shape) != 2:
             raise LoweringError(f"{node.name}: linear expects a [rows, features] input")
         m, k = x.shape
@@ -239,27 +359,85 @@ class _Lowerer:
         self.emit(op)
         self.env[tail] = out
 
+    def _copy_into(self, t: Tensor, label: str) -> Tensor:
+        """A fresh buffer holding `t` (COPY op) — for graph inputs or values
+        already placed in another concat, which cannot alias a concat slice."""
+        out = self.new_tensor(t.shape, dtype=t.dtype)
+        p, c = self._pixels(t)
+        self.emit(LoweredOp(COPY, "copy", OpClass.MEMORY, dict(P=p, C=c, n=1, act=ACT_NONE), [t], out,
+                            bytes_min=2 * self._esz(t) * p * c, label=label))
+        return out
+
     def lower_cat(self, node):
         parts = node.args[0]
         dim = node.args[1] if len(node.args) > 1 else node.kwargs.get("dim", 0)
-        ins = [self.env[p] for p in parts]
-        if any(len(t.shape) != 4 for t in ins) or dim not in (1, -3):
-            raise LoweringError(f"{node.name}: only channel concat of NCHW tensors is supported")
-        n, h, w = ins[0].shape[:3]
-        ctot = sum(t.shape[3] for t in ins)
-        out = self.new_tensor((n, h, w, ctot))
+        ins = [self.value(p) for p in parts]
+        rank = len(ins[0].shape)
+        if any(len(t.shape) != rank for t in ins) or rank not in (2, 4):
+            raise LoweringError(f"{node.name}: concat of 2-D rows or 4-D NCHW maps only")
+        if (rank == 4 and dim not in (1, -3)) or (rank == 2 and dim not in (1, -1)):
+            raise LoweringError(f"{node.name}: only channel / feature concat is supported")
+        lead = ins[0].shape[:-1]
+        if any(t.shape[:-1] != lead for t in ins):
+            raise LoweringError(f"{node.name}: concat inputs disagree outside the channel dim")
+        ctot = sum(t.shape[-1] for t in ins)
+        out = self.new_tensor(tuple(lead) + (ctot,), dtype=ins[0].dtype)
         off = 0
-        for t in ins:
-            if t.alias is not None or t.nchw_input:
-                raise LoweringError(f"{node.name}: concat input already aliased (needs a copy op)")
+        placed = []
+        for p, t in zip(parts, ins):
+            if t.alias is not None or t.nchw_input or t.is_graph_input or t.dtype != out.dtype:
+                t = self._copy_into(t, f"{node.name}.copy")
             t.alias = out
             t.coff_in_alias = off
-            off += t.shape[3]
+            off += t.shape[-1]
+            placed.append(t)
         # The concat stays a DAG node (the paper's operator graph has it) but
         # launches nothing: its producers already wrote their slices, so it is
         # a pure join — capture applies its waits and records only.
-        self.emit(LoweredOp(NOP, "concat", OpClass.MEMORY, {}, ins, out, label=node.name))
+        self.emit(LoweredOp(NOP, "concat", OpClass.MEMORY, {}, placed, out, label=node.name))
         self.env[node] = out
+
+    def lower_add(self, node):
+        """A tree of single-use binary adds (+ an optional sigmoid/ReLU user)
+        becomes one n-ary ADD op (csrc/elementwise.cu)."""
+        leaves = []
+
+        def collect(n):
+            for a in n.args[:2]:
+                if isinstance(a, fx.Node) and self.env.get(a) is _PENDING_ADD:
+                    collect(a)
+                else:
+                    leaves.append(a)
+        collect(node)
+        if len(leaves) > 4:
+            raise LoweringError(f"{node.name}: more than 4 addends")
+        ins = [self.value(a) for a in leaves]
+        shape = ins[0].shape
+        if any(t.shape != shape for t in ins):
+            raise LoweringError(f"{node.name}: broadcasting adds are not supported")
+        tail, act = node, ACT_NONE
+        for pred, code in ((self._is_sigmoid, ACT_SIGMOID), (self._is_relu, ACT_RELU)):
+            u = self._single_user(node, pred)
+            if u is not None:
+                tail, act = u, code
+                self.consumed.add(u)
+                break
+        out = self.new_tensor(shape, dtype=ins[0].dtype)
+        p, c = self._pixels(out)
+        self.emit(LoweredOp(ADD, "add", OpClass.MEMORY, dict(P=p, C=c, n=len(ins), act=act), ins, out,
+                            flops=(len(ins) - 1) * p * c,
+                            bytes_min=(len(ins) + 1) * self._esz(out) * p * c, label=node.name))
+        self.env[tail] = out
+
+    def lower_relu(self, node):
+        lz = self.lazy(node.args[0])
+        self.env[node] = Lazy(lz.tensor, True, lz.sub)
+
+    def lower_subsample(self, node):
+        lz = self.lazy(node.args[0])
+        if lz.sub is not None:
+            raise LoweringError(f"{node.name}: nested subsample")
+        self.env[node] = Lazy(lz.tensor, lz.relu, int(node.args[1]))
 
     # ------------------------------------------------- transformer rows path
     # Token activations are [T, C] row blocks stored as (1, 1, T, C) channel
@@ -274,7 +452,7 @@ class _Lowerer:
         return obj.detach().float().cpu()
 
     def lower_linear_rows(self, node):
-        x = self.env[node.args[0]]
+        x = self.value(node.args[0])
         w = self._param(node.args[1])
         b = self._param(node.args[2]) if len(node.args) > 2 and node.args[2] is not None else None
         n, h, t, k = x.shape
@@ -301,7 +479,7 @@ class _Lowerer:
         self.env[tail] = out
 
     def lower_embeddings(self, node):
-        ids = self.env[node.args[0]]
+        ids = self.value(node.args[0])
         word, pos, typ, gamma, beta = (self._param(a) for a in node.args[1:6])
         eps = float(node.args[6])
         t, c = ids.shape[-1], word.shape[1]
@@ -314,7 +492,7 @@ class _Lowerer:
         self.env[node] = out
 
     def lower_attention(self, node):
-        q, k, v = (self.env[a] for a in node.args[:3])
+        q, k, v = (self.value(a) for a in node.args[:3])
         heads = int(node.args[3])
         t, c = q.shape[2], q.shape[3]
         out = self.new_tensor((1, 1, t, c))
@@ -325,7 +503,7 @@ class _Lowerer:
         self.env[node] = out
 
     def lower_add_layernorm(self, node):
-        x, r = self.env[node.args[0]], self.env[node.args[1]]
+        x, r = self.value(node.args[0]), self.value(node.args[1])
         gamma, beta = self._param(node.args[2]), self._param(node.args[3])
         eps = float(node.args[4])
         t, c = x.shape[2], x.shape[3]
@@ -337,38 +515,92 @@ class _Lowerer:
         self.env[node] = out
 
     def lower_first_token(self, node):
-        x = self.env[node.args[0]]
+        x = self.value(node.args[0])
         view = self.new_tensor((1, 1, 1, x.shape[3]), dtype=x.dtype)
         view.alias, view.coff_in_alias = x, 0   # pixel 0 of x's buffer: a shorter view
         view.producers = set(x.producers)
         self.env[node] = view
 
+    # -------------------------------------------------------- DeepFM path
+
+    def lower_field_embedding(self, node):
+        ids = self.value(node.args[0])
+        field_idx = int(node.args[1])
+        table = self._param(node.args[2])
+        b = ids.shape[0]
+        vocab, dim = table.shape
+        out = self.new_tensor((b, dim), dtype="f32")
+        self.emit(LoweredOp(FIELD_EMBEDDING, "embedding", OpClass.MEMORY,
+                            dict(B=b, dim=dim, field=field_idx, vocab=vocab), [ids], out,
+                            bytes_min=8 * b + 2 * 4 * b * dim, label=node.name,
+                            arrays={"table": table.numpy()}))
+        self.env[node] = out
+
+    def lower_first_order(self, node):
+        ids, w1, dense, wd, bias = node.args[:5]
+        ids_t, dense_t = self.value(ids), self.value(dense)
+        w1a, wda, ba = self._param(w1), self._param(wd), self._param(bias)
+        b = ids_t.shape[0]
+        fields, vocab = w1a.shape
+        out = self.new_tensor((b, 1), dtype="f32")
+        self.emit(LoweredOp(FIRST_ORDER, "gather", OpClass.MEMORY,
+                            dict(B=b, fields=fields, vocab=vocab, n_dense=dense_t.shape[-1]), [ids_t, dense_t], out,
+                            flops=2 * b * (fields + dense_t.shape[-1]),
+                            bytes_min=8 * b * fields + 4 * b * fields + 4 * b * dense_t.shape[-1] + 4 * b,
+                            label=node.name, arrays={"w1": w1a.numpy(), "wd": wda.reshape(-1).numpy()},
+                            floats=(float(ba.reshape(-1)[0]),)))
+        self.env[node] = out
+
+    def lower_fm(self, node):
+        x = self.value(node.args[0])
+        fields = int(node.args[1])
+        b, c = x.shape
+        out = self.new_tensor((b, 1), dtype="f32")
+        self.emit(LoweredOp(FM, "fm", OpClass.MEMORY, dict(B=b, fields=fields, dim=c // fields), [x], out,
+                            flops=3 * b * c, bytes_min=4 * b * c + 4 * b, label=node.name))
+        self.env[node] = out
+
     # ------------------------------------------------------------- driver
 
-    def run(self, example: torch.Tensor) -> Program:
-        token_input = example.dim() == 2 and not example.is_floating_point()
-        if example.dim() != 4 and not token_input:
-            raise LoweringError("example input must be a 4-D NCHW image or a [1, T] token-id tensor")
-        inp = None
+    def _graph_input(self, example: torch.Tensor) -> Tensor:
+        if example.dim() == 4 and example.is_floating_point():
+            n, c, h, w = example.shape
+            t = self.new_tensor((n, h, w, c), dtype="f32")
+            t.nchw_input = True
+        elif not example.is_floating_point():
+            t = self.new_tensor(tuple(example.shape), dtype="i64")
+        elif example.dim() == 2:
+            t = self.new_tensor(tuple(example.shape), dtype="f32")
+        else:
+            raise LoweringError("graph inputs: 4-D NCHW images, 2-D fp32 feature rows or integer ids")
+        t.is_graph_input = True
+        return t
+
+    FUNCTIONS = {
+        "bert_embeddings": "lower_embeddings", "self_attention": "lower_attention",
+        "add_layer_norm": "lower_add_layernorm", "first_token": "lower_first_token",
+        "field_embedding": "lower_field_embedding", "first_order": "lower_first_order",
+        "fm_interaction": "lower_fm", "subsample2d": "lower_subsample",
+    }
+
+    def run(self, examples) -> Program:
+        examples = list(examples) if isinstance(examples, (tuple, list)) else [examples]
+        inputs = []
         for node in self.gm.graph.nodes:
             if node in self.consumed:
                 continue
             if node.op == "placeholder":
-                if inp is not None:
-                    raise LoweringError("single-input models only")
-                if token_input:
-                    inp = self.new_tensor(tuple(example.shape), dtype="i64")
-                else:
-                    n, c, h, w = example.shape
-                    inp = self.new_tensor((n, h, w, c), dtype="f32")
-                    inp.nchw_input = True
-                self.env[node] = inp
+                if len(inputs) >= len(examples):
+                    raise LoweringError("more graph inputs than example tensors")
+                t = self._graph_input(examples[len(inputs)])
+                inputs.append(t)
+                self.env[node] = t
             elif node.op == "get_attr":
                 self.env[node] = None  # parameters are read where they are consumed
             elif node.op == "output":
                 res = node.args[0]
                 outs = list(res) if isinstance(res, (tuple, list)) else [res]
-                self.env["__outs__"] = [self.env[r] for r in outs]
+                self.env["__outs__"] = [self.value(r) for r in outs]
             elif node.op == "call_module":
                 mod = self.gm.get_submodule(node.target)
                 if isinstance(mod, nn.Conv2d):
@@ -389,8 +621,12 @@ class _Lowerer:
                     self.env[node] = self.env[node.args[0]]
                 elif isinstance(mod, nn.Linear):
                     self.lower_linear(node, mod)
+                elif isinstance(mod, nn.ReLU):
+                    self.lower_relu(node)
                 else:
                     raise LoweringError(f"{node.name}: unsupported module {type(mod).__name__}")
+            elif node.op == "call_method" and node.target in ("relu", "relu_"):
+                self.lower_relu(node)
             elif node.op == "call_function":
                 tgt = node.target
                 name = getattr(tgt, "__name__", "")
@@ -398,16 +634,18 @@ class _Lowerer:
                     self.lower_cat(node)
                 elif tgt is F.linear:
                     self.lower_linear_rows(node)
-                elif name == "bert_embeddings":
-                    self.lower_embeddings(node)
-                elif name == "self_attention":
-                    self.lower_attention(node)
-                elif name == "add_layer_norm":
-                    self.lower_add_layernorm(node)
-                elif name == "first_token":
-                    self.lower_first_token(node)
+                elif name in self.FUNCTIONS:
+                    getattr(self, self.FUNCTIONS[name])(node)
+                elif self._is_relu(node):
+                    self.lower_relu(node)
+                elif self._is_add(node):
+                    users = list(node.users)
+                    if len(users) == 1 and self._is_add(users[0]):
+                        self.env[node] = _PENDING_ADD   # folded into its consumer's n-ary ADD
+                    else:
+                        self.lower_add(node)
                 elif tgt is torch.flatten:
-                    x = self.env[node.args[0]]
+                    x = self.value(node.args[0])
                     if len(x.shape) == 2:
                         self.env[node] = x
                     elif len(x.shape) == 4 and x.shape[1] == 1 and x.shape[2] == 1:
@@ -432,12 +670,19 @@ class _Lowerer:
                     d = a[4] if len(a) > 4 else kw.get("dilation", 1)
                     cm = a[5] if len(a) > 5 else kw.get("ceil_mode", False)
                     self.lower_pool(node, True, k, s, p, cm, dilation=d)
+                elif tgt is F.adaptive_avg_pool2d:
+                    size = node.args[1] if len(node.args) > 1 else node.kwargs["output_size"]
+                    if _pair(size) != (1, 1):
+                        raise LoweringError(f"{node.name}: only global adaptive pooling")
+                    self.lower_gap(node)
                 elif tgt in (F.dropout,):
                     self.env[node] = self.env[node.args[0]]
                 else:
                     raise LoweringError(f"{node.name}: unsupported function {tgt}")
             else:
                 raise LoweringError(f"{node.name}: unsupported fx op {node.op}")
+        if len(inputs) != len(examples):
+            raise LoweringError(f"model takes {len(inputs)} inputs, {len(examples)} example tensors given")
         outs = self.env["__outs__"]
         for t in outs:  # graph outputs leave the GEMM engine in fp32
             if t.producers and self.ops[min(t.producers)].kind == CONV2D and t.alias is None:
@@ -447,15 +692,17 @@ class _Lowerer:
             for t in op.inputs:
                 for u in t.producers:
                     edges.add((u, v))
-        return Program(self.ops, self.tensors, inp, outs[0], sorted(edges), outs)
+        return Program(self.ops, self.tensors, inputs[0], outs[0], sorted(edges), outs, inputs)
 
 
-def lower(model: nn.Module, example: torch.Tensor, dtype: str = "f32") -> Program:
+def lower(model: nn.Module, example, dtype: str = "f32") -> Program:
     """Trace `model` with torch.fx and lower it to executor operators.
 
-    dtype "f32": fp32 activations end to end (3xTF32 tensor-core convs).
-    dtype "bf16": bf16 activations and weights with fp32 accumulation; the
-    graph input stays fp32 NCHW and the classifier head stays fp32."""
+    `example` is one input tensor or a tuple of them (one per forward
+    argument).  dtype "f32": fp32 activations end to end (3xTF32 tensor-core
+    convs).  dtype "bf16": bf16 activations and weights with fp32
+    accumulation; the graph input stays fp32 NCHW and the classifier head
+    stays fp32."""
     if dtype not in ("f32", "bf16"):
         raise ValueError(f"unknown dtype {dtype!r}")
     model = model.eval()

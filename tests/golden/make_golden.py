@@ -152,8 +152,10 @@ if __name__ == "__main__" and len(sys.argv) == 1:
 
 
 def model_dags() -> None:
-    """Model DAG fixtures: the GoogLeNet / Inception-v3 DAGs our frontend
-    extracts (static launch-config demands), scheduled by the REFERENCE."""
+    """Model DAG fixtures: the DAGs our frontend extracts for every
+    BASELINE config (GoogLeNet, Inception-v3, NASNet-A Large, BERT-base,
+    DeepFM at batch 1 and 32; static launch-config demands), scheduled by the
+    REFERENCE (its own load_graph / allocate_streams / make_order)."""
     sys.path.insert(0, str(REF))
     sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
     from opsched import GpuConfig, allocate_streams, make_order
@@ -164,9 +166,17 @@ def model_dags() -> None:
 
     cfg = GpuConfig(148, 2048, 233472, 65536, 32)
     out = {}
-    for name in ("googlenet", "inception_v3"):
-        model, x = zoo.build(name)
-        g = engine.static_dag(frontend.lower(model, x))
+    workloads = {
+        "googlenet": lambda: zoo.build("googlenet") + ("f32",),
+        "inception_v3": lambda: zoo.build("inception_v3") + ("f32",),
+        "nasnet_large": lambda: zoo.build("nasnet_large") + ("f32",),
+        "bert_base": lambda: (zoo.build_bert()[0], zoo.build_bert()[2], "bf16"),
+        "deepfm": lambda: zoo.build_deepfm(1) + ("f32",),
+        "deepfm_b32": lambda: zoo.build_deepfm(32) + ("f32",),
+    }
+    for name, make in workloads.items():
+        model, x, dtype = make()
+        g = engine.static_dag(frontend.lower(model, x, dtype))
         d = graph_to_dict(g)
         with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
             json.dump(d, f)

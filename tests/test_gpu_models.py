@@ -94,3 +94,19 @@ def test_bert_base_bf16_parity():
         ref_h, ref_p = ref_model.cuda()(ids.cuda())
     assert _rel(hidden.float().reshape(ref_h.shape), ref_h) < 1e-2
     assert _rel(pooled.float().reshape(ref_p.shape), ref_p) < 1e-2
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-4), ("bf16", 2e-2)])
+def test_nasnet_large_parity(dtype, tol):
+    """NASNet-A Large 331x331 (~700 kernels, ~160 plan streams) through the
+    scheduled graph vs the fp32 eager forward."""
+    from paper_2312_10351_b200 import engine, zoo
+    model, x = zoo.build("nasnet_large")
+    sg = engine.compile(model, x, device=0, profile_reps=1, dtype=dtype)
+    y = sg.run(x.cuda())
+    y_seq = sg.run(x.cuda(), slot=engine.SLOT_SEQUENTIAL)
+    assert torch.equal(y, y_seq)
+    with torch.no_grad():
+        ref = model.cuda()(x.cuda())
+    rel = _rel(y, ref)
+    assert rel <= tol, rel

@@ -114,3 +114,56 @@ def test_concurrency_targets_share_levels():
     prog = frontend.lower(model, x)
     t = engine.concurrency_targets(prog)
     assert t and all(8 <= v <= 148 for v in t.values())
+
+
+def _workload(name):
+    if name == "bert_base":
+        m, _, ids = zoo.build_bert()
+        return m, ids, "bf16"
+    if name.startswith("deepfm"):
+        m, x = zoo.build_deepfm(32 if name.endswith("b32") else 1)
+        return m, x, "f32"
+    m, x = zoo.build(name)
+    return m, x, "f32"
+
+
+@pytest.mark.parametrize("name,v,e,streams", [("nasnet_large", 696, 911, 159), ("bert_base", 110, 157, 25),
+                                              ("deepfm", 36, 36, 29), ("deepfm_b32", 36, 36, 29)])
+def test_new_config_dags_match_fixture(name, v, e, streams):
+    """NASNet-A Large, BERT-base and DeepFM lower to exactly the DAG the
+    reference scheduled for the golden fixture."""
+    model, x, dtype = _workload(name)
+    g = engine.static_dag(frontend.lower(model, x, dtype))
+    d = graph_to_dict(g)
+    gold = MODELS[name]["graph"]
+    assert d["edges"] == gold["edges"]
+    assert [(n["id"], n["name"], n["class"]) for n in d["nodes"]] == \
+           [(n["id"], n["name"], n["class"]) for n in gold["nodes"]]
+    assert (len(g), len(g.edges), op.allocate_streams(g).num_streams) == (v, e, streams)
+
+
+def test_nasnet_relus_are_fused():
+    """Every NASNet ReLU folds into a producer epilogue or a consumer's input
+    (no standalone RELU launches); subsampled factorized-reduction paths fold
+    into stride-2 1x1 convs with padding -offset."""
+    model, x = zoo.build("nasnet_large")
+    prog = frontend.lower(model, x)
+    kinds = [o.kind for o in prog.ops]
+    assert frontend.RELU not in kinds
+    assert sum(1 for o in prog.ops if o.kind == frontend.DWCONV2D and o.ints["relu_in"]) > 50
+    fr = [o for o in prog.ops if o.kind == frontend.CONV2D and o.ints["sh"] == 2 and o.ints["R"] == 1]
+    assert {o.ints["ph"] for o in fr} == {0, -1} and all(o.ints["relu_in"] for o in fr)
+
+
+def test_deepfm_lowering_shape():
+    """26 parallel field gathers write straight into the MLP-input concat; the
+    dense features are copied in; the three heads fold into one sigmoid ADD."""
+    model, x = zoo.build_deepfm(8)
+    prog = frontend.lower(model, x)
+    fields = [o for o in prog.ops if o.kind == frontend.FIELD_EMBEDDING]
+    assert len(fields) == 26
+    offs = sorted(t.root()[1] for o in fields for t in [o.output])
+    assert offs == [13 + 16 * f for f in range(26)]
+    last = prog.ops[-1]
+    assert last.kind == frontend.ADD and last.ints["n"] == 3 and last.ints["act"] == frontend.ACT_SIGMOID
+    assert len(prog.inputs) == 2 and prog.inputs[1].dtype == "i64"
