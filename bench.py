@@ -183,7 +183,8 @@ def run_gpu(args) -> dict | None:
     from paper_2312_10351_b200.dag import graph_to_dict
 
     model, ref_model, x = build_workload(args)
-    sg = engine.compile(model, x, device=local, bound_grids=args.bounded, profile_reps=args.profile_reps,
+    bound = {"auto": "auto", "bounded": True, "full": False}[args.grids]
+    sg = engine.compile(model, x, device=local, bound_grids=bound, profile_reps=args.profile_reps,
                         dtype=args.dtype)
     xd = tuple(t.cuda(local) for t in x) if isinstance(x, tuple) else x.cuda(local)
     # correctness guard on every rank: a fast wrong answer is not a result
@@ -336,9 +337,15 @@ def run_gpu(args) -> dict | None:
         "latency_ms_mean": round(t_par.mean_ms, 4),
         "sequential_latency_ms": round(t_seq.median_ms, 4),
         "speedup_vs_sequential": round(t_seq.median_ms / lat_ms, 4),
+        "grids": "bounded" if sg.bound_grids else "full",
+        "grid_autotune": getattr(sg, "autotune", None),
+        "sequential_best_latency_ms": round(min([t_seq.median_ms] + [a["sequential_ms"] for a in (
+            getattr(sg, "autotune", None) or [])]), 4),
         "latency_warm_l2_ms": round(t_warm.median_ms, 4),
         "sequential_latency_warm_l2_ms": round(t_seq_warm.median_ms, 4),
         "speedup_vs_sequential_warm_l2": round(t_seq_warm.median_ms / t_warm.median_ms, 4),
+        "speedup_vs_best_sequential": round(min([t_seq.median_ms] + [a["sequential_ms"] for a in (
+            getattr(sg, "autotune", None) or [])]) / lat_ms, 4),
         "dag_roofline": {"critical_path_us": round(cp_us, 2), "flop_term_us": round(flop_term_us, 2),
                          "byte_term_us": round(byte_term_us, 2), "roofline_us": round(roof_us, 2),
                          "frac": round(roof_us / (lat_ms * 1e3), 4),
@@ -425,9 +432,9 @@ def main(argv=None) -> int:
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--profile-reps", type=int, default=20,
                     help="launches per op when measuring its isolated in-graph time")
-    ap.add_argument("--bounded", action="store_true",
-                    help="size each conv for its DAG level's share of the SMs (Opara bounded grids) "
-                         "instead of the whole GPU")
+    ap.add_argument("--grids", default="auto", choices=["auto", "bounded", "full"],
+                    help="bounded = size each conv for its DAG level's share of the SMs (Opara bounded "
+                         "grids); full = whole GPU per conv; auto = build both, keep the faster Opara graph")
     args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
     line = run_reference(args) if args.impl == "reference" else run_gpu(args)

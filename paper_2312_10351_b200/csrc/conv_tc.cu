@@ -549,7 +549,7 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   int id = 0, splits = 1;
   const int64_t target = op.i[21] > 0 ? op.i[21] : 148;
   choose_tiling(a, target, (op.variant >= 0 && op.variant < count) ? op.variant : -1,
-                op.i[19] > 1 ? static_cast<int>(op.i[19]) : 0, &id, &splits);
+                op.i[19] > 1 ? static_cast<int>(op.i[19]) : op.i[19] == -1 ? 1 : 0, &id, &splits);
   const void* func = v[id].func[vec ? 1 : 0];
   if (splits > 1 && op.i[19] <= 1) {
     // clusters must be co-resident inside a GPC: keep every cluster in the

@@ -493,7 +493,8 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   const int bn = v[id].bn;
   const int64_t base = static_cast<int64_t>((a.M + bn - 1) / bn) * mtiles;
   const int64_t target = op.i[21] > 0 ? op.i[21] : 148;
-  int64_t splits = op.i[19] > 1 ? op.i[19] : std::max<int64_t>(1, target / base);
+  // i[19]: > 1 forces that split-K, -1 forces none (autotuner), else automatic
+  int64_t splits = op.i[19] > 1 ? op.i[19] : op.i[19] == -1 ? 1 : std::max<int64_t>(1, target / base);
   splits = std::min<int64_t>(splits, kMaxSplits);
   splits = std::min<int64_t>(splits, std::max(1, a.kblocks / 2));
   splits = std::max<int64_t>(1, splits);

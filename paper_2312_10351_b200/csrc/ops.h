@@ -8,7 +8,7 @@
 // CONV2D       i: 0 N, 1 H, 2 W, 3 Cin, 4 in_cstride, 5 in_coff,
 //                 6 OH, 7 OW, 8 Cout, 9 out_cstride, 10 out_coff,
 //                 11 R, 12 S, 13 stride_h, 14 stride_w, 15 pad_h, 16 pad_w,
-//                 17 relu, 18 dtype (0 f32), 19 split_k (1),
+//                 17 relu, 18 dtype (0 f32), 19 split_k (> 1 forced, -1 forced none, else auto),
 //                 20 in_nchw (1: input is a dense NCHW tensor, e.g. the graph input),
 //                 21 target CTAs for split-K (0 = default), 22 engine (0 SIMT fp32,
 //                 1 tcgen05 3xTF32, 2 tcgen05 bf16), 23 output dtype, 24 activation
@@ -16,7 +16,7 @@
 //              p: 0 in, 1 weight: engine 0 [R*S*Cin][Cout] (k = (r*S + s)*Cin + c);
 //                 engine 1 packed tf32 hi/lo UMMA images (conv_tc.cu), 2 bias [Cout], 3 out,
 //                 7 split-K workspace (executor-owned)
-//              variant: tile id, -1 = auto
+//              variant: tile id (tile width 32 << id), -1 = auto
 // MAXPOOL2D /  i: 0 N, 1 H, 2 W, 3 C, 4 in_cstride, 5 in_coff, 6 OH, 7 OW, 8 out_cstride,
 // AVGPOOL2D       9 out_coff, 10 kh, 11 kw, 12 sh, 13 sw, 14 ph, 15 pw,
 //                 16 count_include_pad (avg), 18 dtype

@@ -272,7 +272,7 @@ class ScheduledGraph:
 
     def __init__(self, program: Program, device: int, policy: str = "opara",
                  gpu_config: GpuConfig | None = None, profile_reps: int = 20, seed: int | None = None,
-                 conv_engine: str = "tc", bound_grids: bool = False):
+                 conv_engine: str = "tc", bound_grids: bool = False, tune: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("ScheduledGraph needs a CUDA device (there is no CPU fallback)")
         self.program = program
@@ -283,6 +283,7 @@ class ScheduledGraph:
         self._keep: list[torch.Tensor] = []
         self._alloc(program)
         recs = (_lib.OparaOp * len(program.ops))()
+        self.bound_grids = bool(bound_grids)
         self.targets = concurrency_targets(program) if bound_grids else {}
         for k, op in enumerate(program.ops):
             if op.kind in ROW_KINDS:
@@ -297,6 +298,7 @@ class ScheduledGraph:
                     buf = torch.zeros(4096 + 64, dtype=torch.int64, device=self.dev)
                     self.debug_ts[k] = buf
                     recs[k].p[6] = buf.data_ptr()
+        self.tuning = self._autotune(recs) if tune else {}
         self._recs = recs
         L = _lib.lib()
         h = C.c_void_p()
@@ -377,6 +379,70 @@ class ScheduledGraph:
             self._keep.append(t)
             ptrs.append(t.data_ptr())
         return ptrs
+
+    # ------------------------------------------------------------ tuning
+
+    TUNE_SPLITS = (0, -1, 2, 3, 4, 6, 8)   # 0 = the launcher's own choice, -1 = no split-K
+
+    @staticmethod
+    def _tune_key(rec) -> tuple:
+        """Launch-shape signature of a tensor-core conv record (no pointers)."""
+        return (rec.i[22],) + tuple(rec.i[k] for k in (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15,
+                                                       16, 17, 18, 20, 23, 24, 25))
+
+    def _autotune(self, recs) -> dict:
+        """Pick each tensor-core conv/GEMM's tile width and split-K by
+        measurement: every candidate of every distinct shape is profiled
+        alone (back-to-back in-graph launches, like opara_exec_profile) and
+        the fastest kept.  Under bounded grids only candidates within the
+        op's CTA budget compete.  Returns {op index: (variant, splits, us)}."""
+        L = _lib.lib()
+        groups: dict[tuple, list[int]] = {}
+        for k, op in enumerate(self.program.ops):
+            if op.kind == CONV2D and recs[k].i[22] in (1, 2):
+                groups.setdefault(self._tune_key(recs[k]), []).append(k)
+        cands, owner, seen = [], [], set()
+        for key, ks in groups.items():
+            k0 = ks[0]
+            budget = self.targets.get(k0, 0)
+            for var in range(4):
+                for sp in self.TUNE_SPLITS:
+                    rec = _lib.OparaOp()
+                    C.pointer(rec)[0] = recs[k0]
+                    rec.variant, rec.i[19] = var, sp
+                    prof = _lib.OparaOpProfile()
+                    if L.opara_op_launch_config(C.byref(rec), C.byref(prof)) != 0:
+                        continue
+                    if budget and prof.num_blocks > max(budget, 8):
+                        continue
+                    launch = (key, prof.num_blocks, prof.threads_per_block, prof.shared_mem_per_block)
+                    if launch in seen:   # same effective launch as an earlier candidate
+                        continue
+                    seen.add(launch)
+                    cands.append(rec)
+                    owner.append((key, var, sp, prof.num_blocks))
+        if not cands:
+            return {}
+        arr = (_lib.OparaOp * len(cands))(*cands)
+        h = C.c_void_p()
+        _lib.check(L.opara_exec_create(self.device, C.cast(arr, C.c_void_p), len(cands), C.byref(h)))
+        out = (_lib.OparaOpProfile * len(cands))()
+        try:
+            _lib.check(L.opara_exec_profile(h, 10, C.cast(out, C.c_void_p)))
+        finally:
+            L.opara_exec_destroy(h)
+        best: dict[tuple, tuple] = {}
+        for (key, var, sp, _), p in zip(owner, out):
+            if key not in best or p.isolated_us < best[key][2]:
+                best[key] = (var, sp, p.isolated_us)
+        chosen = {}
+        for key, ks in groups.items():
+            if key in best:
+                var, sp, us = best[key]
+                for k in ks:
+                    recs[k].variant, recs[k].i[19] = var, sp
+                    chosen[k] = (var, sp, us)
+        return chosen
 
     # ---------------------------------------------------- profile / DAG
 
@@ -538,16 +604,40 @@ class ScheduledGraph:
             pass
 
 
-def compile(model: torch.nn.Module, example: torch.Tensor, *, device: int = 0, policy: str = "opara",
+def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "opara",
             dtype: str = "f32",
             gpu_config: GpuConfig | None = None, profile_reps: int = 20,
             seed: int | None = None, conv_engine: str = "tc",
-            bound_grids: bool = False) -> ScheduledGraph:
-    """Model in, scheduled graph out."""
+            bound_grids: bool | str = False, tune: bool = True) -> ScheduledGraph:
+    """Model in, scheduled graph out.
+
+    bound_grids: False = every conv/GEMM sized for the whole GPU; True =
+    Opara's bounded grids (each conv sized for its DAG level's share of the
+    SMs, so concurrent branches co-reside); "auto" = build both, replay each
+    Opara graph and keep the faster one (the other's sequential latency is
+    kept in ``alternative`` for reporting).  tune: pick every tensor-core
+    conv/GEMM's tile width and split-K by measurement (ScheduledGraph._autotune)."""
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     program = lower(model, example, dtype)
-    return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine,
-                          bound_grids)
+    if bound_grids != "auto":
+        return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine,
+                              bool(bound_grids), tune)
+    best, alt = None, {}
+    for bounded in (False, True):
+        sg = ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine, bounded, tune)
+        par = sg.time(SLOT_PARALLEL, warmup=5, iters=30).median_ms
+        seq = sg.time(SLOT_SEQUENTIAL, warmup=5, iters=30).median_ms
+        alt[bounded] = {"bounded": bounded, "parallel_ms": par, "sequential_ms": seq}
+        if best is None or par < best[1]:
+            if best is not None:
+                best[0].close()
+            best = (sg, par)
+        else:
+            sg.close()
+    sg = best[0]
+    sg.alternative = alt[not sg.bound_grids]
+    sg.autotune = [alt[False], alt[True]]
+    return sg
 
 
 def static_dag(program: Program, gpu_config: GpuConfig | None = None,
