@@ -1,4 +1,4 @@
-// Multi-head self-attention for one sequence, one CTA per head, on tcgen05:
+// Multi-head self-attention for one sequence, one CTA (8 warps) per head, on tcgen05:
 //   S = Q K^T          (tcgen05.mma kind::f16, M = 128 queries, N = 128 keys, K = 64)
 //   P = exp((S - max) * scale)   rows in registers straight from TMEM (tcgen05.ld)
 //   O = P V / rowsum   (tcgen05.mma, M = 128 queries, N = 64, K = 128 keys)
@@ -6,7 +6,9 @@
 // columns off + h*64 ..); S and O accumulate in TMEM (fp32).  Operands are
 // staged in 64-byte-swizzled K-major atoms (Q, K by cp.async; V transposed on
 // the way in so the PV MMA reads K-major V^T; P written by the softmax warps).
-// Shapes: tokens = 128, head_dim = 64 (BERT-base at seq 128).
+// Softmax: warps w and w + 4 share TMEM lane quarter w (query rows 32w..32w+31)
+// and split the 128 key columns in halves; row max and row sum are combined
+// through shared memory.  Shapes: tokens = 128, head_dim = 64 (BERT-base, seq 128).
 
 #include <cuda_bf16.h>
 
@@ -18,7 +20,7 @@
 namespace opara {
 namespace {
 
-constexpr int kT = 128, kD = 64, kThreads = 128;
+constexpr int kT = 128, kD = 64, kThreads = 256;
 constexpr uint32_t kQBytes = kT * kD * 2, kKBytes = kT * kD * 2, kPBytes = kT * kT * 2, kVBytes = kD * kT * 2;
 
 struct AttnArgs {
@@ -107,23 +109,29 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
   tc::mbar_wait(&bar[0], 0);
   tc::tc_fence_after();
 
-  // ---- softmax: thread = query row (TMEM lane), 128 scores in registers
-  const int q = warp * 32 + lane;
-  const uint32_t trow = static_cast<uint32_t>(warp * 32) << 16;
-  float sc[kT];
+  // ---- softmax: thread = (query row, half of the key columns), 64 scores in registers
+  __shared__ float red_max[2][kT], red_sum[2][kT];
+  const int quarter = warp & 3, half = warp >> 2;
+  const int q = quarter * 32 + lane;
+  const uint32_t trow = static_cast<uint32_t>(quarter * 32) << 16;
+  constexpr int kHalf = kT / 2;
+  float sc[kHalf];
 #pragma unroll
-  for (int c8 = 0; c8 < kT / 8; ++c8) {
+  for (int c8 = 0; c8 < kHalf / 8; ++c8) {
     float v[8];
-    tc::tmem_ld8(tS + trow + c8 * 8, v);
+    tc::tmem_ld8(tS + trow + half * kHalf + c8 * 8, v);
 #pragma unroll
     for (int e = 0; e < 8; ++e) sc[c8 * 8 + e] = v[e];
   }
   float mx = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < kT; ++j) mx = fmaxf(mx, sc[j]);
+  for (int j = 0; j < kHalf; ++j) mx = fmaxf(mx, sc[j]);
+  red_max[half][q] = mx;
+  __syncthreads();
+  mx = fmaxf(red_max[0][q], red_max[1][q]);
   float sum = 0.f;
 #pragma unroll
-  for (int c16 = 0; c16 < kT / 8; ++c16) {
+  for (int c16 = 0; c16 < kHalf / 8; ++c16) {
     __nv_bfloat16 pv[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -132,11 +140,13 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
       sum += __bfloat162float(pb);  // normalise by exactly what the PV MMA consumes
       pv[e] = pb;
     }
-    *reinterpret_cast<uint4*>(ps + sw64(kT, q, c16)) = *reinterpret_cast<const uint4*>(pv);
+    *reinterpret_cast<uint4*>(ps + sw64(kT, q, half * (kHalf / 8) + c16)) = *reinterpret_cast<const uint4*>(pv);
   }
+  red_sum[half][q] = sum;
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
+  sum = red_sum[0][q] + red_sum[1][q];
 
   // ---- O = P V
   if (tid == 0) {
@@ -151,11 +161,11 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
   tc::mbar_wait(&bar[1], 0);
   tc::tc_fence_after();
   const float inv = 1.f / sum;
-  __nv_bfloat16* og = a.out + static_cast<int64_t>(q) * a.out_stride + a.out_off + h * kD;
+  __nv_bfloat16* og = a.out + static_cast<int64_t>(q) * a.out_stride + a.out_off + h * kD + half * (kD / 2);
 #pragma unroll
-  for (int c8 = 0; c8 < kD / 8; ++c8) {
+  for (int c8 = 0; c8 < kD / 16; ++c8) {
     float v[8];
-    tc::tmem_ld8(tO + trow + c8 * 8, v);
+    tc::tmem_ld8(tO + trow + half * (kD / 2) + c8 * 8, v);
     __nv_bfloat16 ob[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) ob[e] = __float2bfloat16_rn(v[e] * inv);

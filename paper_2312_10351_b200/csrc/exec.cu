@@ -455,6 +455,9 @@ opara_status opara_exec_trace(opara_exec* ex, int32_t slot, void* stream, int64_
     host[2 * i] = ~0ull;
     host[2 * i + 1] = 0ull;
   }
+  // warm replays first: the first launch of a fresh executable graph uploads
+  // it to the device and would stretch the timeline
+  for (int w = 0; w < 3; ++w) OPARA_CUDA(cudaGraphLaunch(g->exec, s));
   OPARA_CUDA(cudaMemcpyAsync(ex->trace_buf, host.data(), sizeof(unsigned long long) * 2 * n,
                              cudaMemcpyHostToDevice, s));
   OPARA_CUDA(cudaGraphLaunch(g->exec, s));

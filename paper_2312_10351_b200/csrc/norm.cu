@@ -110,6 +110,147 @@ __global__ void __launch_bounds__(256) embedding_ln_rows(RowArgs a, unsigned lon
   trace_end(trace);
 }
 
+// ---- 16-byte-vector variants (C % 256 == 0; BERT's 768): lane owns kCh
+// chunks of 8 columns at 8 * (lane + 32 * j).  gamma / beta (and the position
+// / type rows) are parameters, so they are loaded before griddepcontrol.wait,
+// i.e. while the predecessor kernel still runs; after the wait only the
+// activations are read (all of a row's 16-byte loads in flight at once).
+
+__device__ __forceinline__ void bf8_to_f(const uint4& r, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 t = __bfloat1622float2(h[k]);
+    f[2 * k] = t.x;
+    f[2 * k + 1] = t.y;
+  }
+}
+
+template <int kCh>
+struct Affine {
+  float g[kCh][8], b[kCh][8];
+  __device__ __forceinline__ void load(const float* gamma, const float* beta, int lane) {
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) {
+      const int c = 8 * (lane + 32 * j);
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + c));
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + c + 4));
+      g[j][0] = g0.x; g[j][1] = g0.y; g[j][2] = g0.z; g[j][3] = g0.w;
+      g[j][4] = g1.x; g[j][5] = g1.y; g[j][6] = g1.z; g[j][7] = g1.w;
+      b[j][0] = b0.x; b[j][1] = b0.y; b[j][2] = b0.z; b[j][3] = b0.w;
+      b[j][4] = b1.x; b[j][5] = b1.y; b[j][6] = b1.z; b[j][7] = b1.w;
+    }
+  }
+};
+
+template <int kCh>
+__device__ __forceinline__ void ln_store_v(float (&x)[kCh][8], const Affine<kCh>& af, const RowArgs& a, int row,
+                                           int lane) {
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < kCh; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += x[j][e];
+  const float mean = warp_sum(s) / a.C;
+  float v = 0.f;
+#pragma unroll
+  for (int j = 0; j < kCh; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float d = x[j][e] - mean;
+      v += d * d;
+    }
+  const float rstd = rsqrtf(warp_sum(v) / a.C + a.eps);
+  __nv_bfloat16* out = a.out + static_cast<int64_t>(row) * a.out_stride;
+#pragma unroll
+  for (int j = 0; j < kCh; ++j) {
+    uint4 r;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      h[k] = __floats2bfloat162_rn((x[j][2 * k] - mean) * rstd * af.g[j][2 * k] + af.b[j][2 * k],
+                                   (x[j][2 * k + 1] - mean) * rstd * af.g[j][2 * k + 1] + af.b[j][2 * k + 1]);
+    *reinterpret_cast<uint4*>(out + 8 * (lane + 32 * j)) = r;
+  }
+}
+
+template <int kCh>
+__global__ void __launch_bounds__(128) layernorm_rows_v(RowArgs a, unsigned long long* trace) {
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  Affine<kCh> af;
+  af.load(a.gamma, a.beta, lane);
+  pdl_wait();
+  trace_begin(trace);
+  if (row < a.rows) {
+    const __nv_bfloat16* pa = static_cast<const __nv_bfloat16*>(a.a) + static_cast<int64_t>(row) * a.a_stride;
+    const __nv_bfloat16* pb = a.b ? a.b + static_cast<int64_t>(row) * a.b_stride : nullptr;
+    uint4 ra[kCh], rb[kCh];
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) {
+      ra[j] = *reinterpret_cast<const uint4*>(pa + 8 * (lane + 32 * j));
+      if (pb) rb[j] = *reinterpret_cast<const uint4*>(pb + 8 * (lane + 32 * j));
+    }
+    float x[kCh][8];
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) {
+      bf8_to_f(ra[j], x[j]);
+      if (pb) {
+        float y[8];
+        bf8_to_f(rb[j], y);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[j][e] += y[e];
+      }
+    }
+    ln_store_v<kCh>(x, af, a, row, lane);
+  }
+  trace_end(trace);
+}
+
+template <int kCh>
+__global__ void __launch_bounds__(128) embedding_ln_rows_v(RowArgs a, unsigned long long* trace) {
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  Affine<kCh> af;
+  af.load(a.gamma, a.beta, lane);
+  pdl_wait();
+  trace_begin(trace);
+  if (row < a.rows) {
+    const int64_t id = __ldg(a.ids + row);
+    const int64_t tt = a.type_ids ? __ldg(a.type_ids + row) : 0;
+    const float* w = a.word + id * a.C;
+    const float* p = a.pos + static_cast<int64_t>(row + a.pos_off) * a.C;
+    const float* t = a.type + tt * a.C;
+    float4 wv[kCh][2], pv[kCh][2], tv[kCh][2];
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) {
+      const int c = 8 * (lane + 32 * j);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        wv[j][h] = __ldg(reinterpret_cast<const float4*>(w + c) + h);
+        pv[j][h] = __ldg(reinterpret_cast<const float4*>(p + c) + h);
+        tv[j][h] = __ldg(reinterpret_cast<const float4*>(t + c) + h);
+      }
+    }
+    float x[kCh][8];
+#pragma unroll
+    for (int j = 0; j < kCh; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // HF order: (inputs_embeds + token_type) + position
+        x[j][4 * h + 0] = wv[j][h].x + tv[j][h].x + pv[j][h].x;
+        x[j][4 * h + 1] = wv[j][h].y + tv[j][h].y + pv[j][h].y;
+        x[j][4 * h + 2] = wv[j][h].z + tv[j][h].z + pv[j][h].z;
+        x[j][4 * h + 3] = wv[j][h].w + tv[j][h].w + pv[j][h].w;
+      }
+    ln_store_v<kCh>(x, af, a, row, lane);
+  }
+  trace_end(trace);
+}
+
 template <int kPer>
 const void* pick(bool emb) {
   return emb ? reinterpret_cast<const void*>(&embedding_ln_rows<kPer>)
@@ -151,6 +292,23 @@ opara_status launch_rows(const opara_op& op, cudaStream_t s, unsigned long long*
     return fail(OPARA_ERR_VALUE, "layernorm/embedding: C must be a multiple of 64 and <= 1024");
   const int per = a.C / 32;
   LaunchCfg c;
+  const bool aligned = a.C % 256 == 0 && a.out_stride % 8 == 0 && reinterpret_cast<uintptr_t>(a.out) % 16 == 0 &&
+                       (emb || (a.a_stride % 8 == 0 && reinterpret_cast<uintptr_t>(a.a) % 16 == 0 &&
+                                (!a.b || (a.b_stride % 8 == 0 && reinterpret_cast<uintptr_t>(a.b) % 16 == 0))));
+  if (aligned && (a.C == 256 || a.C == 512 || a.C == 768 || a.C == 1024)) {
+    switch (a.C / 256) {
+      case 1: c.func = emb ? (const void*)&embedding_ln_rows_v<1> : (const void*)&layernorm_rows_v<1>; break;
+      case 2: c.func = emb ? (const void*)&embedding_ln_rows_v<2> : (const void*)&layernorm_rows_v<2>; break;
+      case 3: c.func = emb ? (const void*)&embedding_ln_rows_v<3> : (const void*)&layernorm_rows_v<3>; break;
+      default: c.func = emb ? (const void*)&embedding_ln_rows_v<4> : (const void*)&layernorm_rows_v<4>; break;
+    }
+    c.block = dim3(128);
+    c.grid = dim3(ceil_div(a.rows, 4));
+    if (cfg) *cfg = c;
+    if (dry) return OPARA_OK;
+    void* args[] = {&a, &trace};
+    return launch_kernel(c, args, s);
+  }
   switch (per) {
     case 2: c.func = pick<2>(emb); break;
     case 4: c.func = pick<4>(emb); break;

@@ -1,3 +1,5 @@
+import signal
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 import json, sys
 name = sys.argv[1]
 d = json.load(open(f"gpurun_out/profile_{name}.json"))  # name = MODEL_DTYPE[_bounded]
