@@ -207,8 +207,12 @@ def run_gpu(args) -> dict | None:
         dist.barrier()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        if args.profile_region:   # ncu --profile-from-start off: capture only the timed replays
+            torch.cuda.cudart().cudaProfilerStart()
         t_par = sg.time(engine.SLOT_PARALLEL, warmup=args.warmup, iters=args.steps, flush_l2=True)
         torch.cuda.synchronize()
+        if args.profile_region:
+            torch.cuda.cudart().cudaProfilerStop()
     t_seq = sg.time(engine.SLOT_SEQUENTIAL, warmup=args.warmup, iters=args.steps, flush_l2=True)
     t_warm = sg.time(engine.SLOT_PARALLEL, warmup=args.warmup, iters=args.steps, flush_l2=False)
     t_seq_warm = sg.time(engine.SLOT_SEQUENTIAL, warmup=args.warmup, iters=args.steps, flush_l2=False)
@@ -427,6 +431,8 @@ def main(argv=None) -> int:
     ap.add_argument("--model", default="inception_v3",
                     choices=["inception_v3", "googlenet", "bert_base", "nasnet_large", "deepfm"])
     ap.add_argument("--batch", type=int, default=1, help="requests per inference (DeepFM batch sweep 1-32)")
+    ap.add_argument("--profile-region", action="store_true",
+                    help="bracket the timed Opara replays with cudaProfilerStart/Stop (for ncu)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])

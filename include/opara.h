@@ -17,8 +17,10 @@
  *   opara_dominant_share      dominant_share                      orderer.py:45-53
  *   opara_order               order_opara (Alg. 2) / order_baseline("sequential"|"dfs"|
  *                             "wavefront")                        orderer.py:60-153
- *   opara_exec_*              simulate (the "run"), re-designed as a real
- *                             multi-stream CUDA Graph on the B200  simulator.py:212-415
+ *   opara_simulate            simulate (the reference "run": DES model),
+ *                             bit-exact C++ port                  simulator.py:212-415
+ *   opara_exec_*              the same "run" re-designed as a real multi-stream
+ *                             CUDA Graph on the B200 (capture / replay / profile)
  *
  * Status codes map 1:1 onto the reference exception classes (errors.py:4-25);
  * the Python host re-raises the matching class with the message verbatim.
@@ -135,6 +137,31 @@ opara_status opara_dominant_share(const opara_node* node, const opara_gpu_config
 /* Launch order (n node ids).  cfg may be NULL for the non-opara policies. */
 opara_status opara_order(const opara_dag* dag, int32_t policy, const opara_gpu_config* cfg,
                          int64_t* out);
+
+/* -------------------------------------------- execution model (L4) */
+
+typedef struct opara_sim_result {
+  int64_t makespan_ns;
+  int64_t blocked_ns;      /* sum of (first block placed - eligible) */
+  int64_t sync_wait_ns;    /* sum of (eligible - reached stream head) */
+  double sm_efficiency;    /* sum(sm busy) / (num_sms * makespan) */
+} opara_sim_result;
+
+/* The reference's discrete-event multi-SM execution model, bit-exact
+ * (replaces simulate, simulator.py:212-415; semantics simulator.py:1-26).
+ * Per-node arrays are in ascending-id order: block_duration_ns[i]
+ * (OperatorNode.block_duration_ns), stream_of[i].  order = n node ids (a
+ * linear extension), sync_uv = n_sync node-id pairs.  Optional outputs (NULL
+ * to skip): op_start_ns / op_end_ns per node (first block placed / last block
+ * done), sm_busy_ns[num_sms], block_log rows (op id, block index, sm, start,
+ * end) up to block_log_cap rows; *n_blocks receives the placed-block count.
+ * The host checks coverage / plan validity first (CoverageError,
+ * PlanViolationError, InfeasibleBlockError wording of _check_inputs). */
+opara_status opara_simulate(const opara_dag* dag, const int64_t* block_duration_ns, const int32_t* stream_of,
+                            int32_t num_streams, const int64_t* order, const int64_t* sync_uv, int64_t n_sync,
+                            const opara_gpu_config* cfg, opara_sim_result* out, int64_t* op_start_ns,
+                            int64_t* op_end_ns, int64_t* sm_busy_ns, int64_t* block_log, int64_t block_log_cap,
+                            int64_t* n_blocks);
 
 /* ------------------------------------------- executor (subsystems 3 + 4) */
 

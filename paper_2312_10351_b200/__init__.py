@@ -4,7 +4,8 @@ Drop-in for the reference ``opsched`` package's hot path: the same public
 names for the graph model, the stream allocator (Alg. 1) and the launch
 orderer (Alg. 2), computed by the C++ scheduler in libopara.so; and, in place
 of the reference's simulated "run", a real multi-stream CUDA Graph executor
-with hand-written sm_100a kernels (``compile`` / ``ScheduledGraph.run``).
+with hand-written sm_100a kernels (``compile`` / ``ScheduledGraph.run``); the
+simulated run itself is kept as a bit-exact C++ port (``simulate``).
 """
 
 __version__ = "0.1.0"
@@ -20,6 +21,8 @@ from .order import (POLICIES, LaunchSchedule, ResourceScore, dominant_share, loa
                     schedule_to_dict)
 from .plan import (DEFAULT_SYNC_OVERHEAD_US, PlanCost, StreamPlan, allocate_streams, load_plan,
                    plan_to_dict, save_plan, single_stream_plan, validate_plan)
+from .simulator import (BlockRecord, OpRecord, SimResult, result_to_dict, sequential_makespan,
+                        sequential_makespan_ns, simulate, trace, trace_tsv, write_trace)
 
 __all__ = [
     "__version__", "ComputationGraph", "CoverageError", "CudaError", "DEFAULT_GPU",
@@ -30,5 +33,6 @@ __all__ = [
     "gpu_config_to_dict", "graph_from_dict", "graph_to_dict", "load_gpu_config", "load_graph",
     "load_plan", "load_schedule", "make_order", "order_baseline", "order_opara", "plan_to_dict",
     "resource_score", "save_graph", "save_plan", "save_schedule", "schedule_to_dict",
-    "single_stream_plan", "validate_plan",
+    "single_stream_plan", "validate_plan", "BlockRecord", "OpRecord", "SimResult", "result_to_dict",
+    "sequential_makespan", "sequential_makespan_ns", "simulate", "trace", "trace_tsv", "write_trace",
 ]

@@ -65,6 +65,11 @@ class OparaOpProfile(C.Structure):
                 ("isolated_us", C.c_double)]
 
 
+class OparaSimResult(C.Structure):
+    _fields_ = [("makespan_ns", C.c_int64), ("blocked_ns", C.c_int64), ("sync_wait_ns", C.c_int64),
+                ("sm_efficiency", C.c_double)]
+
+
 # Every symbol include/opara.h declares, with its ctypes signature.
 _P = C.c_void_p
 _I64P = C.POINTER(C.c_int64)
@@ -88,6 +93,8 @@ SIGNATURES = {
     "opara_dominant_share": (C.c_int, [C.POINTER(OparaNode), C.POINTER(OparaGpuConfig),
                                        C.POINTER(C.c_double)]),
     "opara_order": (C.c_int, [_P, C.c_int32, C.POINTER(OparaGpuConfig), _P]),
+    "opara_simulate": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, C.c_int64, C.POINTER(OparaGpuConfig),
+                                 C.POINTER(OparaSimResult), _P, _P, _P, _P, C.c_int64, _I64P]),
     "opara_exec_create": (C.c_int, [C.c_int32, _P, C.c_int64, C.POINTER(_P)]),
     "opara_exec_destroy": (None, [_P]),
     "opara_exec_capture": (C.c_int, [_P, C.c_int32, _P, C.c_int32, _P, _P, C.c_int64]),

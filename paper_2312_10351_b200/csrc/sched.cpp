@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "opara.h"
+#include "dag_internal.h"
 #include "status.h"
 
 namespace opara {
@@ -48,17 +49,6 @@ std::string py_pair(int64_t u, int64_t v) {
 
 using opara::fail;
 
-struct opara_dag {
-  std::vector<opara_node> nodes;                 // ascending id
-  std::unordered_map<int64_t, int32_t> index;    // id -> dense index
-  std::vector<int32_t> pred_off, pred;           // CSR, ascending index
-  std::vector<int32_t> succ_off, succ;
-  std::vector<std::pair<int32_t, int32_t>> edges;  // sorted, unique
-  std::vector<int32_t> topo;                     // dense indices
-
-  int32_t n() const { return static_cast<int32_t>(nodes.size()); }
-  int64_t id(int32_t i) const { return nodes[i].id; }
-};
 
 namespace {
 

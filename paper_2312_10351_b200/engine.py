@@ -395,14 +395,23 @@ class ScheduledGraph:
         measurement: every candidate of every distinct shape is profiled
         alone (back-to-back in-graph launches, like opara_exec_profile) and
         the fastest kept.  Under bounded grids only candidates within the
-        op's CTA budget compete.  Returns {op index: (variant, splits, us)}."""
+        op's CTA budget compete.  With OPARA_TUNE_CACHE=<file> the choices
+        persist across compiles (tune once, deploy many).  Returns {op index:
+        (variant, splits, us)}."""
         L = _lib.lib()
         groups: dict[tuple, list[int]] = {}
         for k, op in enumerate(self.program.ops):
             if op.kind == CONV2D and recs[k].i[22] in (1, 2):
-                groups.setdefault(self._tune_key(recs[k]), []).append(k)
+                key = self._tune_key(recs[k]) + (self.targets.get(k, 0),)
+                groups.setdefault(key, []).append(k)
+        cache_path = os.environ.get("OPARA_TUNE_CACHE")
+        cache = {}
+        if cache_path and Path(cache_path).exists():
+            cache = {tuple(json.loads(k)): tuple(v) for k, v in json.loads(Path(cache_path).read_text()).items()}
         cands, owner, seen = [], [], set()
         for key, ks in groups.items():
+            if key in cache:
+                continue
             k0 = ks[0]
             budget = self.targets.get(k0, 0)
             for var in range(4):
@@ -421,20 +430,22 @@ class ScheduledGraph:
                     seen.add(launch)
                     cands.append(rec)
                     owner.append((key, var, sp, prof.num_blocks))
-        if not cands:
-            return {}
-        arr = (_lib.OparaOp * len(cands))(*cands)
-        h = C.c_void_p()
-        _lib.check(L.opara_exec_create(self.device, C.cast(arr, C.c_void_p), len(cands), C.byref(h)))
-        out = (_lib.OparaOpProfile * len(cands))()
-        try:
-            _lib.check(L.opara_exec_profile(h, 10, C.cast(out, C.c_void_p)))
-        finally:
-            L.opara_exec_destroy(h)
-        best: dict[tuple, tuple] = {}
-        for (key, var, sp, _), p in zip(owner, out):
-            if key not in best or p.isolated_us < best[key][2]:
-                best[key] = (var, sp, p.isolated_us)
+        best: dict[tuple, tuple] = {k: v for k, v in cache.items() if k in groups}
+        if cands:
+            arr = (_lib.OparaOp * len(cands))(*cands)
+            h = C.c_void_p()
+            _lib.check(L.opara_exec_create(self.device, C.cast(arr, C.c_void_p), len(cands), C.byref(h)))
+            out = (_lib.OparaOpProfile * len(cands))()
+            try:
+                _lib.check(L.opara_exec_profile(h, 10, C.cast(out, C.c_void_p)))
+            finally:
+                L.opara_exec_destroy(h)
+            for (key, var, sp, _), p in zip(owner, out):
+                if key not in best or p.isolated_us < best[key][2]:
+                    best[key] = (var, sp, p.isolated_us)
+            if cache_path:   # persist: later compiles of the same shapes skip the search
+                cache.update(best)
+                Path(cache_path).write_text(json.dumps({json.dumps(list(k)): list(v) for k, v in cache.items()}))
         chosen = {}
         for key, ks in groups.items():
             if key in best:

@@ -1,9 +1,18 @@
-# ncu evidence for profiles/: launch list of a short bench run + one full capture of the top kernel
+# ncu evidence for profiles/: per workload, the launch list of the bench's timed
+# region (cudaProfilerStart/Stop bracket) and one --set full capture of the
+# dominant kernel family.  Autotune choices are cached first so ncu sees the
+# bench's exact kernels without the tuning launches.
 python __graft_entry__.py || exit 1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_inception_v3.csv \
-    python bench.py --model inception_v3 --steps 2 --warmup 3 --cpu-seconds 0.1 --profile-reps 1 > gpurun_out/ncu_bench.log 2>&1
-echo "launch list rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:conv2d_tc_tf32x3 -s 300 -c 1 -o gpurun_out/conv_tc_full \
-    python bench.py --model inception_v3 --steps 2 --warmup 3 --cpu-seconds 0.1 --profile-reps 1 > gpurun_out/ncu_full.log 2>&1
-echo "full rc=$?"
-tail -n 2 gpurun_out/ncu_full.log
+for spec in "inception_v3 f32 conv2d_tc_tf32x3" "bert_base bf16 conv2d_tc_bf16" "nasnet_large bf16 conv2d_tc_bf16" "googlenet f32 conv2d_tc_tf32x3"; do
+  set -- $spec; m=$1; dt=$2; k=$3
+  export OPARA_TUNE_CACHE=/tmp/tune_${m}_$dt.json
+  python bench.py --model $m --dtype $dt --steps 20 --warmup 3 --cpu-seconds 0.1 > gpurun_out/pre_$m.json 2>/dev/null
+  g=$(python -c "import json;print(json.load(open('gpurun_out/pre_$m.json'))['grids'])")
+  echo "$m $dt grids=$g"
+  timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+     --log-file gpurun_out/launches_${m}_$dt.csv python bench.py --model $m --dtype $dt --grids $g --steps 3 \
+     --warmup 3 --cpu-seconds 0.1 --profile-reps 2 --profile-region > /dev/null 2>&1; echo "launch list rc=$?"
+  timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:$k -s 20 -c 1 \
+     -o gpurun_out/full_${m}_$dt python bench.py --model $m --dtype $dt --grids $g --steps 3 --warmup 3 \
+     --cpu-seconds 0.1 --profile-reps 2 --profile-region > /dev/null 2>&1; echo "full rc=$?"
+done

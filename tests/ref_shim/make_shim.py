@@ -3,10 +3,11 @@
 The reference test suite (/root/reference/pkg/tests, 158 tests) imports
 ``opsched``.  This shim answers those imports with:
 
-* errors / graph / allocator / orderer  ->  paper_2312_10351_b200 (C++ via the C ABI)
-* simulator / oracle / generators / cli / __init__ / __main__  ->  the reference
-  modules themselves (symlinked into a temp dir, never copied into the repo);
-  they are out of the hot path and are the consumers of our outputs.
+* errors / graph / allocator / orderer / simulator  ->  paper_2312_10351_b200
+  (C++ via the C ABI: scheduler, and the bit-exact port of the execution model)
+* oracle / generators / cli / __init__ / __main__  ->  the reference modules
+  themselves (symlinked into a temp dir, never copied into the repo); they are
+  out of the hot path and are the consumers of our outputs.
 
 Used only by tests/test_reference_suite.py in the build container (where
 /root/reference exists).
@@ -40,6 +41,11 @@ def evaluate_plan(g, plan, order, cfg, sync_overhead_us=DEFAULT_SYNC_OVERHEAD_US
                     para_ns / seq_ns if seq_ns else 0.0, cost.sync_count,
                     cost.sync_overhead_us, cost.total_us, para_ns > seq_ns)
 '''
+SIMULATOR = "from paper_2312_10351_b200.simulator import *  # noqa\n" \
+            "from paper_2312_10351_b200.simulator import (BlockRecord, OpRecord, SimResult, TRACE_HEADER,\n" \
+            "    DEFAULT_GPU, GPU_PRESETS, GpuConfig, gpu_config_to_dict, load_gpu_config, result_to_dict,\n" \
+            "    sequential_makespan, sequential_makespan_ns, simulate, trace, trace_tsv, write_trace,\n" \
+            "    _check_inputs, _order_of)\n"
 ORDERER = "from paper_2312_10351_b200.order import (POLICIES, LaunchSchedule, ResourceScore,\n" \
           "    dominant_share, resource_score, order_opara, order_baseline, make_order,\n" \
           "    schedule_to_dict, save_schedule, load_schedule)\n" \
@@ -53,7 +59,8 @@ def make_shim(root: Path) -> Path:
     (pkg / "graph.py").write_text(GRAPH)
     (pkg / "allocator.py").write_text(ALLOCATOR)
     (pkg / "orderer.py").write_text(ORDERER)
-    for name in ("__init__.py", "__main__.py", "simulator.py", "oracle.py", "generators.py", "cli.py"):
+    (pkg / "simulator.py").write_text(SIMULATOR)
+    for name in ("__init__.py", "__main__.py", "oracle.py", "generators.py", "cli.py"):
         link = pkg / name
         if not link.exists():
             os.symlink(REF_SRC / name, link)

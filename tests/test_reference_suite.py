@@ -1,7 +1,8 @@
-"""Run the reference's OWN test suite (158 tests) against our C++ scheduler.
+"""Run the reference's OWN test suite (158 tests) against our C++ scheduler
+and our C++ port of its execution model.
 
 The shim (tests/ref_shim/make_shim.py) routes the reference's graph /
-allocator / orderer imports to paper_2312_10351_b200.  Needs /root/reference,
+allocator / orderer / simulator imports to paper_2312_10351_b200.  Needs /root/reference,
 so it runs in the build container and skips elsewhere (e.g. the GPU box).
 """
 
@@ -38,3 +39,7 @@ def test_reference_suite_passes_against_native_scheduler(tmp_path):
         [sys.executable, "-c", "import opsched, opsched.allocator as a; print(a.allocate_streams.__module__)"],
         capture_output=True, text=True, env=env, cwd=tmp_path)
     assert probe.stdout.strip() == "paper_2312_10351_b200.plan", probe.stderr
+    probe = subprocess.run(
+        [sys.executable, "-c", "import opsched.simulator as s; print(s.simulate.__module__)"],
+        capture_output=True, text=True, env=env, cwd=tmp_path)
+    assert probe.stdout.strip() == "paper_2312_10351_b200.simulator", probe.stderr
