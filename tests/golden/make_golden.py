@@ -19,6 +19,7 @@ threads_per_block, shared_mem_bytes, registers_per_thread, block_duration_us].
 from __future__ import annotations
 
 import json
+import os
 import sys
 import warnings
 from pathlib import Path
@@ -197,3 +198,44 @@ def model_dags() -> None:
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "models":
     model_dags()
+
+
+def cli_fixtures() -> None:
+    """CLI golden outputs: the REFERENCE CLI (python -m opsched) run on two
+    graph files — the 13-node placement cases and the GoogLeNet DAG — with a
+    B200 GpuConfig file; tests/test_cli.py replays our CLI byte for byte."""
+    import shutil
+    import subprocess
+    import tempfile
+    out = OUT.parent / "cli"
+    out.mkdir(exist_ok=True)
+    (out / "b200.json").write_text(json.dumps({"num_sms": 148, "threads_per_sm": 2048,
+                                               "shared_mem_per_sm": 233472, "registers_per_sm": 65536,
+                                               "max_blocks_per_sm": 32, "same_class_slowdown": 1.4},
+                                              indent=2, sort_keys=True) + "\n")
+    env = dict(os.environ, PYTHONPATH=str(REF))
+    gold = json.loads(OUT.with_name("model_dags_golden.json").read_text())
+    (out / "googlenet.json").write_text(json.dumps(gold["googlenet"]["graph"], indent=2, sort_keys=True) + "\n")
+    with tempfile.TemporaryDirectory() as td:
+        subprocess.run([sys.executable, "-m", "opsched", "gen", "cases", "--out", "cases.json"], cwd=td, env=env,
+                       check=True, capture_output=True)
+        shutil.copy(Path(td) / "cases.json", out / "cases.json")
+    for name in ("cases", "googlenet"):
+        with tempfile.TemporaryDirectory() as td:
+            shutil.copy(out / f"{name}.json", Path(td) / "g.json")
+            shutil.copy(out / "b200.json", Path(td) / "b200.json")
+            run = lambda *a: subprocess.run([sys.executable, "-m", "opsched", *a], cwd=td, env=env, check=True,
+                                            capture_output=True, text=True).stdout
+            stdout = run("schedule", "g.json", "--gpu-config", "b200.json")
+            run("simulate", "g.json", "g.plan.json", "g.order.json", "--trace", "g.tsv", "--out", "g.sim.json",
+                "--gpu-config", "b200.json")
+            table = run("compare", "g.json", "--policies", "sequential,opara,dfs,wavefront,random", "--out",
+                        "g.compare.json", "--gpu-config", "b200.json")
+            for suffix in ("plan.json", "order.json", "tsv", "sim.json", "compare.json"):
+                shutil.copy(Path(td) / f"g.{suffix}", out / f"{name}.{suffix}")
+            (out / f"{name}.stdout").write_text(stdout + table)
+    print(f"wrote {out}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "cli":
+    cli_fixtures()
