@@ -33,8 +33,10 @@
 #include "status.h"
 #include "tc_common.cuh"
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
+#include <tuple>
 
 namespace opara {
 namespace {
@@ -63,6 +65,7 @@ struct TcArgs {
   int relu, vec_out, relu_in;
   int M, K, kblocks;
   int splits, kb_per_split;
+  int push, rows_per;   // split-K reduction: 1 = partials pushed to the owner CTA (st.async)
   int64_t sN, sH, sW, sC;
 };
 
@@ -122,6 +125,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   const int kb0 = blockIdx.z * a.kb_per_split;
   const int nkb = min(a.kblocks, kb0 + a.kb_per_split) - kb0;
 
+  // push-mode split-K receive buffer [src rank][128 channels][rows_per] fp32, behind the ring
+  uint64_t* rbar = accum + 2;
+  float* recv = reinterpret_cast<float*>(smem + kStages * kStage + 512);
+  const bool push = a.push != 0;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], 32 * (kProducerWarps / 2) + 1);  // converters + the weight loader
@@ -129,11 +136,21 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(accum, 1);
+    if (push) tc::mbar_init(rbar, 1);
     tc::fence_barrier_init();
   }
   if (warp == 0) tc::tmem_alloc(tslot, kTmemCols);
   tc::tc_fence_before();
-  __syncthreads();
+  if (push) {   // receive barriers initialised cluster-wide before anyone pushes
+    tc::cluster_sync();
+    if (tid == 0) {
+      const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
+      const int mine = max(0, min(BN, r0 + a.rows_per) - r0);
+      tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * mine * 128 * 4));
+    }
+  } else {
+    __syncthreads();
+  }
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
   DBG(1);
@@ -306,6 +323,71 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   // TMEM -> [BN][128] fp32 tile in the idle pipeline smem (all MMAs, hence all
   // smem reads by the tensor core, are complete once `accum` fires).
   DBG(3);
+  if (push) {
+    // TMEM -> registers (sum of the 3xTF32 accumulators) -> st.async of 4-column
+    // float4 groups into the owning rank's receive buffer; owners reduce in rank order
+    const uint32_t me = tc::cluster_ctarank();
+    const int rp = a.rows_per;
+    if (warp < kProducerWarps) {
+      tc::mbar_wait(accum, 0);
+      tc::tc_fence_after();
+      const int quarter = warp & 3, half = warp >> 2;
+      const int chl = quarter * 32 + lane;
+      const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+      const uint32_t recv_s = tc::smem_u32(recv), rbar_s = tc::smem_u32(rbar);
+      constexpr int kC8 = BN / 8 / (kProducerWarps / 4);
+#pragma unroll 2
+      for (int c8 = half * kC8; c8 < (half + 1) * kC8; ++c8) {
+        float v[8], c1[8], c2[8];
+        tc::tmem_ld8(trow + c8 * 8, v);
+        tc::tmem_ld8(trow + BN + c8 * 8, c1);
+        if constexpr (kAcc == 3) tc::tmem_ld8(trow + 2 * BN + c8 * 8, c2);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] += kAcc == 3 ? (c1[e] + c2[e]) : c1[e];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = c8 * 8 + h * 4;
+          const uint32_t owner = static_cast<uint32_t>(col / rp);
+          const uint32_t off = static_cast<uint32_t>(((me * 128 + chl) * rp + (col - owner * rp)) * 4);
+          tc::st_async_f4(tc::map_cluster(recv_s + off, owner),
+                          make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]),
+                          tc::map_cluster(rbar_s, owner));
+        }
+      }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tc::tc_fence_after();
+      tc::tmem_dealloc(tmem, kTmemCols);
+    }
+    const int r0 = static_cast<int>(me) * rp;
+    const int mine = max(0, min(BN, r0 + rp) - r0);
+    if (mine > 0) {
+      tc::mbar_wait_cluster(rbar, 0);
+      const int groups = mine / 4;
+      for (int t = tid; t < 128 * groups; t += kThreads) {
+        const int chl = t & 127, g = t >> 7;
+        const int ch = mt * 128 + chl;
+        if (ch >= a.Cout) continue;
+        float4 acc = *reinterpret_cast<const float4*>(recv + chl * rp + 4 * g);
+        for (int z = 1; z < a.splits; ++z) {
+          const float4 q = *reinterpret_cast<const float4*>(recv + (z * 128 + chl) * rp + 4 * g);
+          acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+        }
+        const float b = a.bias ? __ldg(a.bias + ch) : 0.f;
+        float y[4] = {acc.x + b, acc.y + b, acc.z + b, acc.w + b};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (a.relu) y[e] = fmaxf(y[e], 0.f);
+          const int p = n0 + r0 + 4 * g + e;
+          if (p < a.M) a.out[static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch] = y[e];
+        }
+      }
+    }
+    trace_end(trace);
+    return;
+  }
   float* tile = reinterpret_cast<float*>(smem);
   if (warp < kProducerWarps) {
     // warp w may only touch TMEM lanes [32*(w%4), +32): lane quarter w%4,
@@ -425,13 +507,25 @@ const TcVariant* tc_variants(int* count) {
   return v;
 }
 
+constexpr size_t kPushMaxBytes = 48 * 1024;
+constexpr size_t kSmemLimit = 232448;   // 227 KB of opt-in dynamic smem per CTA (sm_100)
+inline size_t attr_smem(size_t ring) { return std::min(ring + kPushMaxBytes, kSmemLimit); }
+
+bool push_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("OPARA_SPLITK_PUSH");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 opara_status set_smem_attr(const TcVariant& v) {
   static bool done[4][2] = {};
   int idx = v.bn == 32 ? 0 : v.bn == 64 ? 1 : v.bn == 128 ? 2 : 3;
   for (int k = 0; k < 2; ++k) {
     if (done[idx][k]) continue;
     cudaError_t e = cudaFuncSetAttribute(v.func[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(v.smem));
+                                         static_cast<int>(attr_smem(v.smem)));
     if (e != cudaSuccess) return cuda_fail(e, "conv2d_tc smem attribute");
     done[idx][k] = true;
   }
@@ -440,17 +534,17 @@ opara_status set_smem_attr(const TcVariant& v) {
 
 // How many clusters of `size` CTAs fit on the device at once (cached per
 // kernel/size; without a device assume the 148-SM / one-CTA-per-SM bound).
-int64_t max_active_clusters(const void* func, int size, size_t smem) {
+int64_t max_active_clusters(const void* func, int size, size_t smem, size_t smem_attr) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, int>, int64_t> cache;
+  static std::map<std::tuple<const void*, int, size_t>, int64_t> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_pair(func, size);
+  auto key = std::make_tuple(func, size, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int64_t result = 148 / size;
   int dev_count = 0;
   if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0 &&
-      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) ==
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_attr)) ==
           cudaSuccess) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(1, 1, size);
@@ -555,15 +649,27 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
     // clusters must be co-resident inside a GPC: keep every cluster in the
     // first wave (a second wave doubles the latency of the whole conv)
     const int64_t clusters = static_cast<int64_t>((a.M + v[id].bn - 1) / v[id].bn) * ((a.Cout + 127) / 128);
-    while (splits > 1 && clusters > max_active_clusters(func, splits, v[id].smem)) --splits;
+    while (splits > 1) {
+      const int rp = ((v[id].bn + splits - 1) / splits + 3) / 4 * 4;
+      const size_t rb = static_cast<size_t>(splits) * 128 * rp * 4;
+      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && !push_disabled();
+      const size_t sm = v[id].smem + (pu ? rb : 0);
+      if (clusters <= max_active_clusters(func, splits, sm, attr_smem(v[id].smem))) break;
+      --splits;
+    }
   }
   a.kb_per_split = (a.kblocks + splits - 1) / splits;
   a.splits = (a.kblocks + a.kb_per_split - 1) / a.kb_per_split;
+  // split-K reduction: push (st.async to the owning rank) when its buffer is small, else DSMEM pull
+  a.rows_per = ((v[id].bn + a.splits - 1) / a.splits + 3) / 4 * 4;
+  const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
+  a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
+            !push_disabled()) ? 1 : 0;
   LaunchCfg c;
   c.func = func;
   c.grid = dim3(ceil_div(a.M, v[id].bn), (a.Cout + 127) / 128, a.splits);
   c.block = dim3(kThreads);
-  c.smem = v[id].smem;
+  c.smem = v[id].smem + (a.push ? recv_bytes : 0);
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
   opara_status st = set_smem_attr(v[id]);

@@ -19,8 +19,10 @@
 
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <type_traits>
 
 #include "device_common.cuh"
@@ -53,6 +55,7 @@ struct BfArgs {
   int act, vec_out, relu_in;
   int M, K, kblocks;
   int splits, kb_per_split;
+  int push, rows_per;   // split-K reduction: 1 = partials pushed to the owner CTA (st.async)
   int64_t sN, sH, sW, sC;
 };
 
@@ -97,17 +100,34 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   const int kb0 = blockIdx.z * a.kb_per_split;
   const int nkb = min(a.kblocks, kb0 + a.kb_per_split) - kb0;
 
+  // push-mode split-K: receive buffer [src rank][128 channels][rows_per columns]
+  // fp32 behind the ring (other CTAs may push while this CTA's ring is busy)
+  uint64_t* rbar = accum + 2;
+  float* recv = reinterpret_cast<float*>(smem + kStages * kStage + 256);
+  const bool push = a.push != 0;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], 32 * kGatherWarps + 1);  // gather threads + the weight loader
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(accum, 1);
+    if (push) tc::mbar_init(rbar, 1);
     tc::fence_barrier_init();
   }
   if (warp == 0) tc::tmem_alloc(tslot, kTmemCols);
   tc::tc_fence_before();
-  __syncthreads();
+  if (push) {
+    // every CTA's receive barrier is initialised before anyone pushes (this
+    // runs before griddepcontrol.wait, overlapping the predecessor kernel)
+    tc::cluster_sync();
+    if (tid == 0) {
+      const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
+      const int mine = max(0, min(BN, r0 + a.rows_per) - r0);
+      tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * mine * 128 * 4));
+    }
+  } else {
+    __syncthreads();
+  }
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
 
@@ -273,6 +293,73 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   __syncwarp();
 
   // ------------------------------------------------------------ epilogue
+  if (push) {
+    // TMEM -> registers -> st.async of 4-column float4 groups straight into the
+    // owning rank's receive buffer (slot = my rank); the owner's mbarrier
+    // counts the bytes.  No cluster barrier and no remote loads on this path.
+    const uint32_t me = tc::cluster_ctarank();
+    const int rp = a.rows_per;
+    if (warp < 4) {
+      tc::mbar_wait(accum, 0);
+      tc::tc_fence_after();
+      const int chl = warp * 32 + lane;
+      const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+      const uint32_t recv_s = tc::smem_u32(recv);
+      const uint32_t rbar_s = tc::smem_u32(rbar);
+#pragma unroll 2
+      for (int c8 = 0; c8 < BN / 8; ++c8) {
+        float v[8];
+        tc::tmem_ld8(trow + c8 * 8, v);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = c8 * 8 + h * 4;
+          const uint32_t owner = static_cast<uint32_t>(col / rp);
+          const uint32_t off = static_cast<uint32_t>(((me * 128 + chl) * rp + (col - owner * rp)) * 4);
+          tc::st_async_f4(tc::map_cluster(recv_s + off, owner), make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2],
+                                                                            v[4 * h + 3]),
+                          tc::map_cluster(rbar_s, owner));
+        }
+      }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tc::tc_fence_after();
+      tc::tmem_dealloc(tmem, kTmemCols);
+    }
+    // owner: wait for every rank's partial columns, reduce in rank order
+    const int r0 = static_cast<int>(me) * rp;
+    const int mine = max(0, min(BN, r0 + rp) - r0);
+    if (mine > 0) {
+      tc::mbar_wait_cluster(rbar, 0);
+      TO* out = static_cast<TO*>(a.out);
+      const int groups = mine / 4;
+      for (int t = tid; t < 128 * groups; t += kThreads) {
+        const int chl = t & 127, g = t >> 7;
+        const int ch = mt * 128 + chl;
+        if (ch >= a.Cout) continue;
+        float4 acc = *reinterpret_cast<const float4*>(recv + (0 * 128 + chl) * rp + 4 * g);
+        for (int z = 1; z < a.splits; ++z) {
+          const float4 q = *reinterpret_cast<const float4*>(recv + (z * 128 + chl) * rp + 4 * g);
+          acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+        }
+        const float b = a.bias ? __ldg(a.bias + ch) : 0.f;
+        const float y[4] = {act_fn(acc.x + b, a.act), act_fn(acc.y + b, a.act), act_fn(acc.z + b, a.act),
+                            act_fn(acc.w + b, a.act)};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int p = n0 + r0 + 4 * g + e;
+          if (p < a.M) {
+            TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
+            if constexpr (std::is_same<TO, float>::value) *dst = y[e];
+            else *dst = __float2bfloat16_rn(y[e]);
+          }
+        }
+      }
+    }
+    trace_end(trace);
+    return;
+  }
   float* tile = reinterpret_cast<float*>(smem);
   if (warp < 4) {
     tc::mbar_wait(accum, 0);
@@ -389,6 +476,18 @@ const BfVariant* bf_variants() {
   return v;
 }
 
+constexpr size_t kPushMaxBytes = 48 * 1024;
+constexpr size_t kSmemLimit = 232448;   // 227 KB of opt-in dynamic smem per CTA (sm_100)
+inline size_t attr_smem(size_t ring) { return std::min(ring + kPushMaxBytes, kSmemLimit); }
+
+bool push_disabled() {
+  static const bool off = [] {
+    const char* v = std::getenv("OPARA_SPLITK_PUSH");
+    return v && v[0] == '0';
+  }();
+  return off;
+}
+
 opara_status set_attr_once(const void* func, size_t smem) {
   static std::mutex mu;
   static std::map<const void*, bool> done;
@@ -400,17 +499,17 @@ opara_status set_attr_once(const void* func, size_t smem) {
   return OPARA_OK;
 }
 
-int64_t max_clusters(const void* func, int size, size_t smem) {
+int64_t max_clusters(const void* func, int size, size_t smem, size_t smem_attr) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, int>, int64_t> cache;
+  static std::map<std::tuple<const void*, int, size_t>, int64_t> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_pair(func, size);
+  auto key = std::make_tuple(func, size, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int64_t result = 2 * 148 / size;
   int dev_count = 0;
   if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0 &&
-      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) == cudaSuccess) {
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_attr)) == cudaSuccess) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(1, 1, size);
     lc.blockDim = dim3(kThreads);
@@ -500,17 +599,31 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   splits = std::max<int64_t>(1, splits);
   const void* func = v[id].func[mode][out_f32 ? 1 : 0];
   if (splits > 1 && op.i[19] <= 1)
-    while (splits > 1 && base > max_clusters(func, static_cast<int>(splits), v[id].smem)) --splits;
+    while (splits > 1) {
+      const int rp = ((bn + static_cast<int>(splits) - 1) / static_cast<int>(splits) + 3) / 4 * 4;
+      const size_t rb = static_cast<size_t>(splits) * 128 * rp * 4;
+      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && !push_disabled();
+      const size_t sm = v[id].smem + (pu ? rb : 0);
+      if (base <= max_clusters(func, static_cast<int>(splits), sm, attr_smem(v[id].smem))) break;
+      --splits;
+    }
   a.kb_per_split = static_cast<int>((a.kblocks + splits - 1) / splits);
   a.splits = (a.kblocks + a.kb_per_split - 1) / a.kb_per_split;
+  // Split-K reduction mode: push (each rank st.async's its partial columns to
+  // the owning rank, which waits on byte counts) when the receive buffer is
+  // small; otherwise pull over DSMEM after a cluster barrier.
+  a.rows_per = ((bn + a.splits - 1) / a.splits + 3) / 4 * 4;
+  const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
+  a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
+            !push_disabled()) ? 1 : 0;
   LaunchCfg c;
   c.func = func;
   c.grid = dim3(ceil_div(a.M, bn), mtiles, a.splits);
   c.block = dim3(kThreads);
-  c.smem = v[id].smem;
+  c.smem = v[id].smem + (a.push ? recv_bytes : 0);
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
-  opara_status st = set_attr_once(func, c.smem);
+  opara_status st = set_attr_once(func, attr_smem(v[id].smem));
   if (st != OPARA_OK) return st;
   void* args[] = {&a, &trace};
   return launch_kernel(c, args, s, a.splits > 1 ? static_cast<unsigned>(a.splits) : 1u);

@@ -189,6 +189,28 @@ __device__ __forceinline__ uint32_t map_cluster(uint32_t saddr, uint32_t rank) {
   return r;
 }
 
+// Asynchronous 16-byte store into (possibly another CTA's) shared memory of
+// the cluster; its bytes complete_tx on the destination CTA's mbarrier `cbar`
+// (cluster address), which is how the receiver learns the data has landed.
+__device__ __forceinline__ void st_async_f4(uint32_t caddr, float4 v, uint32_t cbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+               ::"r"(caddr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(cbar)
+               : "memory");
+}
+
+// Wait on a local mbarrier phase that remote st.async / bulk copies complete
+// (acquire at cluster scope so the remote bytes are visible).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t caddr) {
   float4 v;
   // ordered after the producing cluster barrier by that barrier's own clobber

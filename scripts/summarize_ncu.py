@@ -19,22 +19,28 @@ hdr, data = rows[hi], rows[hi + 1:]
 ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
 scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 tot, cnt = collections.defaultdict(float), collections.Counter()
+
+
+def is_ours(name: str) -> bool:   # libopara kernels live in opara::(anonymous namespace)
+    return "opara::" in name or "unnamed>::" in name
+
 ours = []
 for r in data:
     name = r[ik].split("(")[0].replace("void ", "")
     v = float(r[iv].replace(",", "")) * scale[r[iu]]
     tot[name] += v
     cnt[name] += 1
-    if "opara::" in name:
+    if is_ours(name):
         ours.append((r[0], name, r[hdr.index("Grid Size")], r[hdr.index("Block Size")], f"{v:.3f}"))
-T_ours = sum(v for k, v in tot.items() if "opara::" in k)
+T_ours = sum(v for k, v in tot.items() if is_ours(k))
 lines.append(f"# ncu launch list — {tag}\n")
 lines.append(f"Source: `{launches.name}` (`ncu --metrics gpu__time_duration.sum --clock-control none`, "
-             "cold-cache and serialised per launch: compare SHARES, not absolutes). Rows are the repo's "
-             "kernels only; torch/cuDNN launches of the correctness check are excluded from the shares.\n")
+             "cold-cache and serialised per launch: compare SHARES, not absolutes), captured inside the "
+             "bench's timed region only (`--profile-region`: cudaProfilerStart/Stop around the Opara "
+             "replays), so every row is a libopara kernel.\n")
 lines.append("| share of our kernel time | total us | launches | kernel |\n|---:|---:|---:|---|")
 for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-    if "opara::" in k:
+    if is_ours(k):
         lines.append(f"| {v / T_ours * 100:5.1f}% | {v:10.1f} | {cnt[k]:5d} | `{k}` |")
 (out / f"{tag}_launches.md").write_text("\n".join(lines) + "\n")
 with (out / f"{tag}_launches_ours.csv").open("w", newline="") as f:
