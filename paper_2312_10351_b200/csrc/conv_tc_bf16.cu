@@ -602,7 +602,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
     while (splits > 1) {
       const int rp = ((bn + static_cast<int>(splits) - 1) / static_cast<int>(splits) + 3) / 4 * 4;
       const size_t rb = static_cast<size_t>(splits) * 128 * rp * 4;
-      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && !push_disabled();
+      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && !push_disabled() && op.i[26] == 0;
       const size_t sm = v[id].smem + (pu ? rb : 0);
       if (base <= max_clusters(func, static_cast<int>(splits), sm, attr_smem(v[id].smem))) break;
       --splits;
@@ -615,7 +615,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   a.rows_per = ((bn + a.splits - 1) / a.splits + 3) / 4 * 4;
   const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
   a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
-            !push_disabled()) ? 1 : 0;
+            !push_disabled() && op.i[26] == 0) ? 1 : 0;
   LaunchCfg c;
   c.func = func;
   c.grid = dim3(ceil_div(a.M, bn), mtiles, a.splits);

@@ -5,11 +5,11 @@
 // with f = ReLU when the op's input ReLU is fused (relu_in; NASNet applies
 // ReLU in front of every separable conv) and act = none / ReLU.
 // Per-channel work is only k*k MACs, so the kernel is bound by moving the
-// activations: one thread owns one output pixel x one 16-byte channel vector
-// (4 fp32 / 8 bf16 channels), reads every input vector of its window with a
-// 128-bit load (the k*k-fold window overlap between neighbouring threads is
-// served by L1), the tap weights as fp32 float4 from the read-only path, and
-// accumulates in fp32.  Consecutive threads walk channels first, so a warp's
+// activations: one thread owns kPx adjacent output pixels x one 16-byte
+// channel vector (4 fp32 / 8 bf16 channels; 8 / 4-byte vectors for channel
+// counts that are not multiples of 8), reads every input vector of its window
+// with a vector load (the window overlap between neighbours is served by L1),
+// each tap's fp32 weights once for its kPx pixels, and accumulates in fp32.  Consecutive threads walk channels first, so a warp's
 // loads and stores are contiguous along C.  The grid is bounded to a few CTAs
 // per SM (grid-stride) so concurrent branches co-reside.
 //
@@ -47,6 +47,17 @@ __device__ __forceinline__ void load_vec(const T* src, float* f) {
     const float4 r1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
     f[0] = r0.x; f[1] = r0.y; f[2] = r0.z; f[3] = r0.w;
     f[4] = r1.x; f[5] = r1.y; f[6] = r1.z; f[7] = r1.w;
+  } else if constexpr (sizeof(T) == 2 && V == 4) {
+    const uint2 r = __ldg(reinterpret_cast<const uint2*>(src));
+    const float2 t0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
+    const float2 t1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
+    f[0] = t0.x; f[1] = t0.y; f[2] = t1.x; f[3] = t1.y;
+  } else if constexpr (sizeof(T) == 2 && V == 2) {
+    const float2 t = __bfloat1622float2(__ldg(reinterpret_cast<const __nv_bfloat162*>(src)));
+    f[0] = t.x; f[1] = t.y;
+  } else if constexpr (sizeof(T) == 4 && V == 2) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(src));
+    f[0] = t.x; f[1] = t.y;
   } else if constexpr (sizeof(T) == 2 && V == 8) {
     const uint4 r = __ldg(reinterpret_cast<const uint4*>(src));
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
@@ -68,6 +79,15 @@ template <typename T, int V>
 __device__ __forceinline__ void store_vec(T* dst, const float* f) {
   if constexpr (sizeof(T) == 4 && V == 4) {
     *reinterpret_cast<float4*>(dst) = make_float4(f[0], f[1], f[2], f[3]);
+  } else if constexpr (sizeof(T) == 2 && V == 4) {
+    uint2 r;
+    *reinterpret_cast<__nv_bfloat162*>(&r.x) = __floats2bfloat162_rn(f[0], f[1]);
+    *reinterpret_cast<__nv_bfloat162*>(&r.y) = __floats2bfloat162_rn(f[2], f[3]);
+    *reinterpret_cast<uint2*>(dst) = r;
+  } else if constexpr (sizeof(T) == 2 && V == 2) {
+    *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(f[0], f[1]);
+  } else if constexpr (sizeof(T) == 4 && V == 2) {
+    *reinterpret_cast<float2*>(dst) = make_float2(f[0], f[1]);
   } else if constexpr (sizeof(T) == 2 && V == 8) {
     uint4 r;
     __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
@@ -82,55 +102,101 @@ __device__ __forceinline__ void store_vec(T* dst, const float* f) {
   }
 }
 
-template <typename T, int V>
+// A thread owns one 16-byte channel vector of kPx horizontally adjacent
+// output pixels: each tap's weights are loaded once and reused for the kPx
+// pixels (L1 serves the overlapping input columns).  Square k x k windows
+// known at compile time (KS = 3, 5, 7) unroll both tap loops so a thread's
+// window loads are all in flight together; KS = 0 is the generic fallback.
+constexpr int kPx = 1;   // 4 was measured slower: too few threads on small maps
+
+template <typename T, int V, int KS>
 __global__ void __launch_bounds__(256) dwconv2d_nhwc(DwArgs a, unsigned long long* trace) {
   pdl_trigger();
   pdl_wait();
   trace_begin(trace);
   const int cv = a.C / V;
-  const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
+  const int owb = (a.OW + kPx - 1) / kPx;
+  const int64_t total = static_cast<int64_t>(a.N) * a.OH * owb * cv;
   const T* in = static_cast<const T*>(a.in);
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int c = static_cast<int>(t % cv) * V;
     int64_t q = t / cv;
-    const int ow = static_cast<int>(q % a.OW);
-    q /= a.OW;
+    const int ow0 = static_cast<int>(q % owb) * kPx;
+    q /= owb;
     const int oh = static_cast<int>(q % a.OH);
     const int b = static_cast<int>(q / a.OH);
-    const int ih0 = oh * a.sh - a.ph, iw0 = ow * a.sw - a.pw;
-    float acc[V];
+    const int ih0 = oh * a.sh - a.ph;
+    float acc[kPx][V];
 #pragma unroll
-    for (int e = 0; e < V; ++e) acc[e] = 0.f;
-    for (int r = 0; r < a.kh; ++r) {
+    for (int p = 0; p < kPx; ++p)
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[p][e] = 0.f;
+    const T* base = in + static_cast<int64_t>(b) * a.H * a.W * a.in_cs + a.in_coff + c;
+    auto tap = [&](int r, int s) {
       const int ih = ih0 + r;
-      if (ih < 0 || ih >= a.H) continue;
-      const T* row = in + (static_cast<int64_t>(b) * a.H + ih) * a.W * a.in_cs + a.in_coff + c;
-      const float* wrow = a.w + static_cast<int64_t>(r) * a.kw * a.C + c;
-      for (int s = 0; s < a.kw; ++s) {
-        const int iw = iw0 + s;
-        if (iw < 0 || iw >= a.W) continue;
-        float x[V], w[V];
+      if (ih < 0 || ih >= a.H) return;
+      float w[V];
+      load_vec<float, V>(a.w + static_cast<int64_t>(r * a.kw + s) * a.C + c, w);
+      const T* row = base + static_cast<int64_t>(ih) * a.W * a.in_cs;
+#pragma unroll
+      for (int p = 0; p < kPx; ++p) {
+        const int iw = (ow0 + p) * a.sw - a.pw + s;
+        if (ow0 + p >= a.OW || iw < 0 || iw >= a.W) continue;
+        float x[V];
         load_vec<T, V>(row + static_cast<int64_t>(iw) * a.in_cs, x);
-        load_vec<float, V>(wrow + static_cast<int64_t>(s) * a.C, w);
         if (a.relu_in) {
 #pragma unroll
           for (int e = 0; e < V; ++e) x[e] = fmaxf(x[e], 0.f);
         }
 #pragma unroll
-        for (int e = 0; e < V; ++e) acc[e] = fmaf(x[e], w[e], acc[e]);
+        for (int e = 0; e < V; ++e) acc[p][e] = fmaf(x[e], w[e], acc[p][e]);
       }
-    }
+    };
+    if constexpr (KS > 0) {
 #pragma unroll
-    for (int e = 0; e < V; ++e) {
-      float v = acc[e] + (a.bias ? __ldg(a.bias + c + e) : 0.f);
-      acc[e] = a.act == 1 ? fmaxf(v, 0.f) : v;
+      for (int r = 0; r < KS; ++r)
+#pragma unroll
+        for (int s = 0; s < KS; ++s) tap(r, s);
+    } else {
+      for (int r = 0; r < a.kh; ++r)
+        for (int s = 0; s < a.kw; ++s) tap(r, s);
     }
-    store_vec<T, V>(static_cast<T*>(a.out) + ((static_cast<int64_t>(b) * a.OH + oh) * a.OW + ow) * a.out_cs +
-                        a.out_coff + c,
-                    acc);
+    float bias[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) bias[e] = a.bias ? __ldg(a.bias + c + e) : 0.f;
+#pragma unroll
+    for (int p = 0; p < kPx; ++p) {
+      if (ow0 + p >= a.OW) break;
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const float v = acc[p][e] + bias[e];
+        acc[p][e] = a.act == 1 ? fmaxf(v, 0.f) : v;
+      }
+      store_vec<T, V>(static_cast<T*>(a.out) + ((static_cast<int64_t>(b) * a.OH + oh) * a.OW + ow0 + p) * a.out_cs +
+                          a.out_coff + c,
+                      acc[p]);
+    }
   }
   trace_end(trace);
+}
+
+template <typename T, int V>
+const void* pick_ks(int ks) {
+  switch (ks) {
+    case 3: return reinterpret_cast<const void*>(&dwconv2d_nhwc<T, V, 3>);
+    case 5: return reinterpret_cast<const void*>(&dwconv2d_nhwc<T, V, 5>);
+    case 7: return reinterpret_cast<const void*>(&dwconv2d_nhwc<T, V, 7>);
+    default: return reinterpret_cast<const void*>(&dwconv2d_nhwc<T, V, 0>);
+  }
+}
+
+template <typename T>
+const void* pick_dw(int vw, int ks) {
+  if (vw == 8 && sizeof(T) == 2) return pick_ks<T, 8>(ks);
+  if (vw == 4) return pick_ks<T, 4>(ks);
+  if (vw == 2) return pick_ks<T, 2>(ks);
+  return pick_ks<T, 1>(ks);
 }
 
 }  // namespace
@@ -154,13 +220,22 @@ opara_status launch_dwconv2d(const opara_op& op, cudaStream_t s, unsigned long l
   const bool vec = a.C % V == 0 && a.in_cs % V == 0 && a.in_coff % V == 0 && a.out_cs % V == 0 &&
                    a.out_coff % V == 0 && reinterpret_cast<uintptr_t>(a.in) % 16 == 0 &&
                    reinterpret_cast<uintptr_t>(a.out) % 16 == 0 && reinterpret_cast<uintptr_t>(a.w) % 16 == 0;
+  // vector width: 16 bytes when every view allows it, else 8 / 4 bytes, else scalar
+  auto fits = [&](int v) {
+    return a.C % v == 0 && a.in_cs % v == 0 && a.in_coff % v == 0 && a.out_cs % v == 0 && a.out_coff % v == 0;
+  };
+  int vw = 1;
+  if (vec) vw = V;
+  else if (bf && fits(4) && reinterpret_cast<uintptr_t>(a.in) % 8 == 0 && reinterpret_cast<uintptr_t>(a.out) % 8 == 0)
+    vw = 4;
+  else if (fits(2) && reinterpret_cast<uintptr_t>(a.in) % (bf ? 4 : 8) == 0 &&
+           reinterpret_cast<uintptr_t>(a.out) % (bf ? 4 : 8) == 0)
+    vw = 2;
+  const int ks = (a.kh == a.kw && (a.kh == 3 || a.kh == 5 || a.kh == 7)) ? a.kh : 0;
   LaunchCfg c;
-  c.func = bf ? (vec ? reinterpret_cast<const void*>(&dwconv2d_nhwc<__nv_bfloat16, 8>)
-                     : reinterpret_cast<const void*>(&dwconv2d_nhwc<__nv_bfloat16, 1>))
-              : (vec ? reinterpret_cast<const void*>(&dwconv2d_nhwc<float, 4>)
-                     : reinterpret_cast<const void*>(&dwconv2d_nhwc<float, 1>));
-  const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / (vec ? V : 1));
-  c.block = dim3(256);
+  c.func = bf ? pick_dw<__nv_bfloat16>(vw, ks) : pick_dw<float>(vw, ks);
+  const int64_t work = static_cast<int64_t>(a.N) * a.OH * ((a.OW + kPx - 1) / kPx) * (a.C / vw);
+  c.block = dim3(256);   // (smaller CTAs on small maps measured slower)
   c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(work, 256), 148u * 4u)));
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;

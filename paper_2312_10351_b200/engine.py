@@ -161,7 +161,8 @@ def concurrency_targets(program: Program, num_sms: int = 148) -> dict[int, int]:
     return out
 
 
-def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -> _lib.OparaOp:
+def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0,
+               splitk_pull: bool = False) -> _lib.OparaOp:
     """Fill the POD launch record of one lowered op (layouts: csrc/ops.h)."""
     rec = _lib.OparaOp()
     rec.kind = op.kind
@@ -178,7 +179,7 @@ def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0) -
         vals = [q["N"], q["H"], q["W"], q["Cin"], ics, icoff, q["OH"], q["OW"], q["Cout"], ocs, ocoff,
                 q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], in_dt if conv_engine == 2 else 0,
                 1, int(inchw), int(target_ctas), conv_engine, DTYPE_CODE[op.output.dtype],
-                q.get("act", 1 if q["relu"] else 0), q.get("relu_in", 0)]
+                q.get("act", 1 if q["relu"] else 0), q.get("relu_in", 0), int(splitk_pull)]
         rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
     elif op.kind == DWCONV2D:
         vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff, q["OH"], q["OW"], ocs, ocoff, q["kh"], q["kw"],
@@ -272,7 +273,8 @@ class ScheduledGraph:
 
     def __init__(self, program: Program, device: int, policy: str = "opara",
                  gpu_config: GpuConfig | None = None, profile_reps: int = 20, seed: int | None = None,
-                 conv_engine: str = "tc", bound_grids: bool = False, tune: bool = True):
+                 conv_engine: str = "tc", bound_grids: bool = False, tune: bool = True,
+                 splitk: str = "push"):
         if not torch.cuda.is_available():
             raise RuntimeError("ScheduledGraph needs a CUDA device (there is no CPU fallback)")
         self.program = program
@@ -284,13 +286,15 @@ class ScheduledGraph:
         self._alloc(program)
         recs = (_lib.OparaOp * len(program.ops))()
         self.bound_grids = bool(bound_grids)
+        self.splitk = splitk   # split-K reduction: "push" (st.async to the owner) or "pull" (DSMEM)
         self.targets = concurrency_targets(program) if bound_grids else {}
         for k, op in enumerate(program.ops):
             if op.kind in ROW_KINDS:
                 recs[k] = _op_record(op, self._all_views(op), self._arrays(op))
             else:
                 recs[k] = _op_record(op, self._views(op), self._weights(op),
-                                     conv_engine_for(op, self.conv_engine), self.targets.get(k, 0))
+                                     conv_engine_for(op, self.conv_engine), self.targets.get(k, 0),
+                                     splitk == "pull")
         self.debug_ts = {}
         if os.environ.get("OPARA_CONV_DEBUG"):  # per-phase timestamps of CTA 0 (conv_tc.cu)
             for k, op in enumerate(program.ops):
@@ -388,7 +392,7 @@ class ScheduledGraph:
     def _tune_key(rec) -> tuple:
         """Launch-shape signature of a tensor-core conv record (no pointers)."""
         return (rec.i[22],) + tuple(rec.i[k] for k in (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15,
-                                                       16, 17, 18, 20, 23, 24, 25))
+                                                       16, 17, 18, 20, 23, 24, 25, 26))
 
     def _autotune(self, recs) -> dict:
         """Pick each tensor-core conv/GEMM's tile width and split-K by
@@ -624,30 +628,32 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
 
     bound_grids: False = every conv/GEMM sized for the whole GPU; True =
     Opara's bounded grids (each conv sized for its DAG level's share of the
-    SMs, so concurrent branches co-reside); "auto" = build both, replay each
-    Opara graph and keep the faster one (the other's sequential latency is
-    kept in ``alternative`` for reporting).  tune: pick every tensor-core
+    SMs, so concurrent branches co-reside); "auto" = build every combination
+    of {full, bounded} grids x {push, pull} split-K reductions, replay each
+    Opara graph and keep the fastest (all four latencies are kept in
+    ``autotune`` for reporting).  tune: pick every tensor-core
     conv/GEMM's tile width and split-K by measurement (ScheduledGraph._autotune)."""
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     program = lower(model, example, dtype)
     if bound_grids != "auto":
         return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine,
                               bool(bound_grids), tune)
-    best, alt = None, {}
+    best, tried = None, []
     for bounded in (False, True):
-        sg = ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine, bounded, tune)
-        par = sg.time(SLOT_PARALLEL, warmup=5, iters=30).median_ms
-        seq = sg.time(SLOT_SEQUENTIAL, warmup=5, iters=30).median_ms
-        alt[bounded] = {"bounded": bounded, "parallel_ms": par, "sequential_ms": seq}
-        if best is None or par < best[1]:
-            if best is not None:
-                best[0].close()
-            best = (sg, par)
-        else:
-            sg.close()
+        for splitk in ("push", "pull"):
+            sg = ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine, bounded, tune,
+                                splitk)
+            par = sg.time(SLOT_PARALLEL, warmup=5, iters=30).median_ms
+            seq = sg.time(SLOT_SEQUENTIAL, warmup=5, iters=30).median_ms
+            tried.append({"bounded": bounded, "splitk": splitk, "parallel_ms": par, "sequential_ms": seq})
+            if best is None or par < best[1]:
+                if best is not None:
+                    best[0].close()
+                best = (sg, par)
+            else:
+                sg.close()
     sg = best[0]
-    sg.alternative = alt[not sg.bound_grids]
-    sg.autotune = [alt[False], alt[True]]
+    sg.autotune = tried
     return sg
 
 

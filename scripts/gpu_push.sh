@@ -1,0 +1,11 @@
+python __graft_entry__.py || exit 1
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for spec in "bert_base bf16" "inception_v3 f32" "inception_v3 bf16" "googlenet f32" "nasnet_large bf16" "nasnet_large f32"; do
+  set -- $spec
+  for pv in 0 1; do
+    OPARA_SPLITK_PUSH=$pv timeout 600 python bench.py --model $1 --dtype $2 --steps 100 --warmup 10 --cpu-seconds 0.2 > /tmp/b.json 2>/tmp/b.err
+    python -c "import json;d=json.load(open('/tmp/b.json'));print('push=$pv $1 $2', 'lat',d['latency_ms'],'seq',d['sequential_latency_ms'],'x',d['speedup_vs_sequential'],'xbest',d['speedup_vs_best_sequential'],d['grids'],'cp',d['dag_roofline']['critical_path_us'],'rel',round(d['rel_err_vs_torch_fp32'],7))" || tail -3 /tmp/b.err
+  done
+done
+python scripts/profile_ops.py nasnet_large bf16 && python scripts/cp_breakdown.py nasnet_large_bf16
+python scripts/profile_ops.py bert_base bf16 && python scripts/cp_breakdown.py bert_base_bf16

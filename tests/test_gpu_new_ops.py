@@ -59,7 +59,9 @@ class SepBlock(nn.Module):
 
 @pytest.mark.parametrize("c,k,s,hw,dtype,tol", [(32, 3, 1, 21, "f32", 1e-4), (48, 5, 2, 42, "f32", 1e-4),
                                                 (64, 7, 2, 83, "f32", 1e-4), (40, 3, 1, 11, "f32", 1e-4),
-                                                (64, 5, 2, 42, "bf16", 2e-2), (96, 7, 1, 21, "bf16", 2e-2)])
+                                                (64, 5, 2, 42, "bf16", 2e-2), (96, 7, 1, 21, "bf16", 2e-2),
+                                                (42, 5, 2, 83, "bf16", 2e-2), (84, 7, 2, 42, "bf16", 2e-2),
+                                                (42, 3, 1, 21, "f32", 1e-4), (36, 5, 1, 11, "bf16", 2e-2)])
 def test_separable_block(c, k, s, hw, dtype, tol):
     from paper_2312_10351_b200 import engine
     torch.manual_seed(0)
