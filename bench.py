@@ -277,8 +277,8 @@ def run_gpu(args) -> dict | None:
         achieved = d["bytes"] / (d["us"] * 1e-6) / 1e9
         peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
     traffic = None
-    prof = ROOT / "profiles" / f"r01_{args.model}_full.md"
-    if prof.exists() and dom == "conv2d_tc_tf32x3":
+    prof = ROOT / "profiles" / f"r01_{args.model}_{args.dtype}_full.md"
+    if prof.exists() and dom in prof.read_text():
         vals = {}
         for ln in prof.read_text().splitlines():
             parts = [x.strip() for x in ln.split("|")]
@@ -298,8 +298,8 @@ def run_gpu(args) -> dict | None:
                         "nominal fp32 FFMA (148 SM x 128 lanes x 2 x 1.965 GHz)" if unit == "TFLOP/s"
                         else "measured HBM copy (MEASURED_PEAKS.json)"),
         "traffic": traffic,
-        "traffic_note": "dram read+write bytes of one launch from the committed ncu --set full capture "
-                        "(cold cache under ncu)" if traffic else None,
+        "traffic_note": f"dram read+write bytes of one {dom} launch from the committed ncu --set full capture "
+                        f"({prof.name}, cold cache under ncu)" if traffic else None,
         "share_of_step": round(d["us"] / total_us, 3),
         "launches_per_step": d["launches"],
         "flops_per_step": d["flops"],
