@@ -138,18 +138,33 @@ def pack_conv_weights_tf32x3(wk: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(np.stack([image(hi), image(lo)], axis=2)).reshape(-1)
 
 
+def dag_levels(program: Program) -> list[int]:
+    """Longest-path depth of every op (ops are emitted in topological order)."""
+    preds = [[] for _ in program.ops]
+    for u, v in program.edges:
+        preds[v].append(u)
+    level = [0] * len(program.ops)
+    for v in range(len(program.ops)):
+        level[v] = 1 + max((level[u] for u in preds[v]), default=-1)
+    return level
+
+
+def concurrent_convs(program: Program) -> dict[int, int]:
+    """Per conv/GEMM op: how many convs/GEMMs share its DAG level (can run beside it)."""
+    level = dag_levels(program)
+    count: dict[int, int] = {}
+    for v, op in enumerate(program.ops):
+        if op.kind == CONV2D:
+            count[level[v]] = count.get(level[v], 0) + 1
+    return {v: count[level[v]] for v, op in enumerate(program.ops) if op.kind == CONV2D}
+
+
 def concurrency_targets(program: Program, num_sms: int = 148) -> dict[int, int]:
     """CTA budget per conv: the SMs are shared among the convs of the same DAG
     level (longest-path depth) in proportion to their FLOPs, so branches that
     can run concurrently are sized to co-reside instead of each claiming the
     whole GPU (Opara's bounded grids)."""
-    n = len(program.ops)
-    preds = [[] for _ in range(n)]
-    for u, v in program.edges:
-        preds[v].append(u)
-    level = [0] * n
-    for v in range(n):  # ops are emitted in topological order
-        level[v] = 1 + max((level[u] for u in preds[v]), default=-1)
+    level = dag_levels(program)
     work: dict[int, int] = {}
     for v, op in enumerate(program.ops):
         if op.kind == CONV2D:
@@ -286,7 +301,13 @@ class ScheduledGraph:
         self._alloc(program)
         recs = (_lib.OparaOp * len(program.ops))()
         self.bound_grids = bool(bound_grids)
-        self.splitk = splitk   # split-K reduction: "push" (st.async to the owner) or "pull" (DSMEM)
+        # split-K reduction: "push" (st.async partials to the owner CTA), "pull" (DSMEM after a
+        # cluster barrier), or "auto": pull where other convs share the DAG level (concurrent
+        # branches), push for convs that run alone
+        self.splitk = splitk
+        conc = concurrent_convs(program) if splitk == "auto" else {}
+        pull_of = {k: (splitk == "pull") or (splitk == "auto" and conc.get(k, 1) > 1)
+                   for k in range(len(program.ops))}
         self.targets = concurrency_targets(program) if bound_grids else {}
         for k, op in enumerate(program.ops):
             if op.kind in ROW_KINDS:
@@ -294,7 +315,7 @@ class ScheduledGraph:
             else:
                 recs[k] = _op_record(op, self._views(op), self._weights(op),
                                      conv_engine_for(op, self.conv_engine), self.targets.get(k, 0),
-                                     splitk == "pull")
+                                     pull_of[k])
         self.debug_ts = {}
         if os.environ.get("OPARA_CONV_DEBUG"):  # per-phase timestamps of CTA 0 (conv_tc.cu)
             for k, op in enumerate(program.ops):
@@ -629,8 +650,8 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
     bound_grids: False = every conv/GEMM sized for the whole GPU; True =
     Opara's bounded grids (each conv sized for its DAG level's share of the
     SMs, so concurrent branches co-reside); "auto" = build every combination
-    of {full, bounded} grids x {push, pull} split-K reductions, replay each
-    Opara graph and keep the fastest (all four latencies are kept in
+    of {full, bounded} grids x {push, pull, auto} split-K reductions, replay
+    each Opara graph and keep the fastest (all latencies are kept in
     ``autotune`` for reporting).  tune: pick every tensor-core
     conv/GEMM's tile width and split-K by measurement (ScheduledGraph._autotune)."""
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
@@ -640,7 +661,7 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
                               bool(bound_grids), tune)
     best, tried = None, []
     for bounded in (False, True):
-        for splitk in ("push", "pull"):
+        for splitk in ("push", "pull", "auto"):
             sg = ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine, bounded, tune,
                                 splitk)
             par = sg.time(SLOT_PARALLEL, warmup=5, iters=30).median_ms
