@@ -124,6 +124,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   const int mt = blockIdx.y;        // 128-channel tile
   const int kb0 = blockIdx.z * a.kb_per_split;
   const int nkb = min(a.kblocks, kb0 + a.kb_per_split) - kb0;
+#ifndef OPARA_BIAS_LATE
+  // pull-epilogue bias (lane = 4 channels): a parameter, fetched before griddepcontrol.wait
+  const int ch = mt * 128 + lane * 4;
+  float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (a.bias && !a.push) {
+    if (ch + 0 < a.Cout) bias4.x = __ldg(a.bias + ch + 0);
+    if (ch + 1 < a.Cout) bias4.y = __ldg(a.bias + ch + 1);
+    if (ch + 2 < a.Cout) bias4.z = __ldg(a.bias + ch + 2);
+    if (ch + 3 < a.Cout) bias4.w = __ldg(a.bias + ch + 3);
+  }
+#endif
 
   // push-mode split-K receive buffer [src rank][128 channels][rows_per] fp32, behind the ring
   uint64_t* rbar = accum + 2;
@@ -424,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   const int rank = splits > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
   const int rows_per = (BN + splits - 1) / splits;
   const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
+#ifdef OPARA_BIAS_LATE
   const int ch = mt * 128 + lane * 4;
   float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
   if (a.bias) {
@@ -432,6 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     if (ch + 2 < a.Cout) bias4.z = __ldg(a.bias + ch + 2);
     if (ch + 3 < a.Cout) bias4.w = __ldg(a.bias + ch + 3);
   }
+#endif
   const uint32_t tile_s = tc::smem_u32(tile);
   for (int row = r0 + warp; row < r1; row += kThreads / 32) {
     const int p = n0 + row;

@@ -99,6 +99,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   const int mt = blockIdx.y;
   const int kb0 = blockIdx.z * a.kb_per_split;
   const int nkb = min(a.kblocks, kb0 + a.kb_per_split) - kb0;
+#ifndef OPARA_BIAS_LATE
+  // the pull epilogue's bias (lane = 4 channels) is a parameter: fetch it now,
+  // before griddepcontrol.wait, so its latency hides under the predecessor
+  const int ch = mt * 128 + lane * 4;
+  float bias[4] = {0.f, 0.f, 0.f, 0.f};
+  if (a.bias && !a.push) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (ch + e < a.Cout) bias[e] = __ldg(a.bias + ch + e);
+  }
+#endif
 
   // push-mode split-K: receive buffer [src rank][128 channels][rows_per columns]
   // fp32 behind the ring (other CTAs may push while this CTA's ring is busy)
@@ -382,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   const int rank = splits > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
   const int rows_per = (BN + splits - 1) / splits;
   const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
+#ifdef OPARA_BIAS_LATE
   const int ch = mt * 128 + lane * 4;
   float bias[4] = {0.f, 0.f, 0.f, 0.f};
   if (a.bias) {
@@ -389,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     for (int e = 0; e < 4; ++e)
       if (ch + e < a.Cout) bias[e] = __ldg(a.bias + ch + e);
   }
+#endif
   const uint32_t tile_s = tc::smem_u32(tile);
   TO* out = static_cast<TO*>(a.out);
   for (int row = r0 + warp; row < r1; row += kThreads / 32) {

@@ -644,7 +644,8 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
             dtype: str = "f32",
             gpu_config: GpuConfig | None = None, profile_reps: int = 20,
             seed: int | None = None, conv_engine: str = "tc",
-            bound_grids: bool | str = False, tune: bool = True) -> ScheduledGraph:
+            bound_grids: bool | str = False, tune: bool = True,
+            splitk: str | None = None) -> ScheduledGraph:
     """Model in, scheduled graph out.
 
     bound_grids: False = every conv/GEMM sized for the whole GPU; True =
@@ -653,12 +654,16 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
     of {full, bounded} grids x {push, pull, auto} split-K reductions, replay
     each Opara graph and keep the fastest (all latencies are kept in
     ``autotune`` for reporting).  tune: pick every tensor-core
-    conv/GEMM's tile width and split-K by measurement (ScheduledGraph._autotune)."""
+    conv/GEMM's tile width and split-K by measurement (ScheduledGraph._autotune).
+    splitk: split-K reduction ("push" / "pull" / "auto", see ScheduledGraph) for
+    a fixed grid policy; default pull with bounded grids, push with full grids."""
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     program = lower(model, example, dtype)
     if bound_grids != "auto":
+        # measured default: pull reductions pair with bounded grids, push with full grids
+        splitk = splitk or ("pull" if bound_grids else "push")
         return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine,
-                              bool(bound_grids), tune)
+                              bool(bound_grids), tune, splitk)
     best, tried = None, []
     for bounded in (False, True):
         for splitk in ("push", "pull", "auto"):
