@@ -72,22 +72,24 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
 
   pdl_wait();
   trace_begin(trace);
-  // ---- stage Q, K (cp.async) and V^T (register transpose)
+  // ---- stage Q, K (cp.async) and V (registers, all loads in flight at once);
+  // S = Q K^T is issued as soon as Q and K land, and V is transposed into the
+  // K-major V^T operand while the tensor core works on S.
   const __nv_bfloat16* qg = a.q + a.q_off + h * kD;
   const __nv_bfloat16* kg = a.k + a.k_off + h * kD;
   const __nv_bfloat16* vg = a.v + a.v_off + h * kD;
-  for (int u = tid; u < kT * (kD / 8); u += kThreads) {
-    const int row = u >> 3, c16 = u & 7;
+  constexpr int kChunks = kT * (kD / 8) / kThreads;   // 16-byte chunks per thread per operand
+#pragma unroll
+  for (int j = 0; j < kChunks; ++j) {
+    const int u = tid + j * kThreads, row = u >> 3, c16 = u & 7;
     cp_async16(tc::smem_u32(qs) + sw64(kT, row, c16), qg + static_cast<int64_t>(row) * a.q_stride + c16 * 8);
     cp_async16(tc::smem_u32(ks) + sw64(kT, row, c16), kg + static_cast<int64_t>(row) * a.k_stride + c16 * 8);
   }
-  for (int u = tid; u < kT * (kD / 8); u += kThreads) {
-    const int key = u >> 3, d0 = (u & 7) * 8;
-    const uint4 raw = *reinterpret_cast<const uint4*>(vg + static_cast<int64_t>(key) * a.v_stride + d0);
-    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&raw);
+  uint4 vraw[kChunks];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)  // V^T[d][key]: row d, k = key
-      *reinterpret_cast<__nv_bfloat16*>(vt + sw64(kD, d0 + i, key >> 3) + (key & 7) * 2) = e[i];
+  for (int j = 0; j < kChunks; ++j) {
+    const int u = tid + j * kThreads, key = u >> 3, d0 = (u & 7) * 8;
+    vraw[j] = *reinterpret_cast<const uint4*>(vg + static_cast<int64_t>(key) * a.v_stride + d0);
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   tc::fence_proxy_async_smem();
@@ -105,6 +107,14 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
                   tc::smem_desc_sw64(tc::smem_u32(ks) + off, 512), kIdS, s != 0);
     }
     tc::mma_commit(&bar[0]);
+  }
+#pragma unroll
+  for (int j = 0; j < kChunks; ++j) {
+    const int u = tid + j * kThreads, key = u >> 3, d0 = (u & 7) * 8;
+    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&vraw[j]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)  // V^T[d][key]: row d, k = key
+      *reinterpret_cast<__nv_bfloat16*>(vt + sw64(kD, d0 + i, key >> 3) + (key & 7) * 2) = e[i];
   }
   tc::mbar_wait(&bar[0], 0);
   tc::tc_fence_after();
