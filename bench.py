@@ -47,7 +47,8 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampled every 200 ms while the timed region runs."""
+    """nvidia-smi sampled every 100 ms while the timed region (plus untimed
+    replays around it, so short regions are covered) runs."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -62,7 +63,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -206,6 +207,12 @@ def run_gpu(args) -> dict | None:
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clk:
+        # keep the GPU busy with (untimed) replays for ~0.6 s before and ~0.3 s
+        # after the timed region so the 100 ms nvidia-smi sampler sees it loaded
+        lat0 = sg.time(engine.SLOT_PARALLEL, warmup=1, iters=5, flush_l2=False).median_ms
+        roll = min(20000, max(1, int(600.0 / max(lat0, 0.01))))   # ~0.6 s of replays
+        if not args.profile_region:
+            sg.time(engine.SLOT_PARALLEL, warmup=0, iters=roll, flush_l2=False)
         torch.cuda.synchronize()
         if args.profile_region:   # ncu --profile-from-start off: capture only the timed replays
             torch.cuda.cudart().cudaProfilerStart()
@@ -213,6 +220,9 @@ def run_gpu(args) -> dict | None:
         torch.cuda.synchronize()
         if args.profile_region:
             torch.cuda.cudart().cudaProfilerStop()
+        else:
+            sg.time(engine.SLOT_PARALLEL, warmup=0, iters=max(1, roll // 2), flush_l2=False)
+            torch.cuda.synchronize()
     t_seq = sg.time(engine.SLOT_SEQUENTIAL, warmup=args.warmup, iters=args.steps, flush_l2=True)
     t_warm = sg.time(engine.SLOT_PARALLEL, warmup=args.warmup, iters=args.steps, flush_l2=False)
     t_seq_warm = sg.time(engine.SLOT_SEQUENTIAL, warmup=args.warmup, iters=args.steps, flush_l2=False)
