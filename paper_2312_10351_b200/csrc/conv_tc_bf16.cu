@@ -40,7 +40,13 @@ constexpr int kThreads = 192;
 constexpr int kMaxSplits = 8;
 constexpr uint32_t kWBytes = 128 * kBK * 2;  // 8 KB
 
-__host__ __device__ constexpr int bf_stages(int bn) { return bn <= 64 ? 8 : 6; }
+// Ring depth per tile width.  The 16-wide tile keeps a 24-deep ring (216 KB):
+// one CTA per SM can hold a whole K = 768 weight slice, all of it fetched
+// before griddepcontrol.wait (weights do not depend on the predecessor), so
+// after the wait only the small activation tile is on the critical path.
+__host__ __device__ constexpr int bf_stages(int bn) { return bn == 16 ? 24 : bn <= 64 ? 8 : 6; }
+// full[], empty[], accum, tmem slot, push barrier: rounded up to 128 bytes
+__host__ __device__ constexpr int bf_bar_bytes(int stages) { return ((2 * stages + 3) * 8 + 127) / 128 * 128; }
 
 enum GatherMode { kVecBf16 = 0, kScalarBf16 = 1, kScalarF32 = 2 };
 
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   // push-mode split-K: receive buffer [src rank][128 channels][rows_per columns]
   // fp32 behind the ring (other CTAs may push while this CTA's ring is busy)
   uint64_t* rbar = accum + 2;
-  float* recv = reinterpret_cast<float*>(smem + kStages * kStage + 256);
+  float* recv = reinterpret_cast<float*>(smem + kStages * kStage + bf_bar_bytes(kStages));
   const bool push = a.push != 0;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
 
 template <int BN>
 constexpr size_t bf_smem_bytes() {
-  return bf_stages(BN) * (kWBytes + static_cast<size_t>(BN) * kBK * 2) + 256 + 1024;
+  return bf_stages(BN) * (kWBytes + static_cast<size_t>(BN) * kBK * 2) + bf_bar_bytes(bf_stages(BN)) + 1024;
 }
 
 struct BfVariant {
@@ -485,7 +491,7 @@ BfVariant make_bf() {
 }
 
 const BfVariant* bf_variants() {
-  static const BfVariant v[] = {make_bf<32>(), make_bf<64>(), make_bf<128>(), make_bf<256>()};
+  static const BfVariant v[] = {make_bf<32>(), make_bf<64>(), make_bf<128>(), make_bf<256>(), make_bf<16>()};
   return v;
 }
 
@@ -591,7 +597,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   const BfVariant* v = bf_variants();
   const int mtiles = (a.Cout + 127) / 128;
   int id = op.variant;
-  if (id < 0 || id > 3) {
+  if (id < 0 || id > 4) {   // 0..3: tile width 32 << id, 4: width 16 (deep weight ring)
     id = 0;
     const int bns[4] = {32, 64, 128, 256};
     for (int k = 3; k >= 0; --k) {

@@ -439,7 +439,7 @@ class ScheduledGraph:
                 continue
             k0 = ks[0]
             budget = self.targets.get(k0, 0)
-            for var in range(4):
+            for var in range(4):   # tile widths 32 << var (the 16-wide deep-ring tile hogs an SM: explicit only)
                 for sp in self.TUNE_SPLITS:
                     rec = _lib.OparaOp()
                     C.pointer(rec)[0] = recs[k0]
