@@ -21,6 +21,8 @@
 
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "device_common.cuh"
 #include "ops.h"
 #include "status.h"
@@ -67,6 +69,29 @@ __device__ __forceinline__ void load_vec(const T* src, float* f) {
       f[2 * k] = t.x;
       f[2 * k + 1] = t.y;
     }
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      if constexpr (sizeof(T) == 2) f[e] = __bfloat162float(src[e]); else f[e] = src[e];
+    }
+  }
+}
+
+// Plain (generic / shared-memory) vector load: 16-byte bf16x8 or fp32x4.
+template <typename T, int V>
+__device__ __forceinline__ void load_vec_plain(const T* src, float* f) {
+  if constexpr (sizeof(T) == 2 && V == 8) {
+    const uint4 r = *reinterpret_cast<const uint4*>(src);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 t = __bfloat1622float2(h[k]);
+      f[2 * k] = t.x;
+      f[2 * k + 1] = t.y;
+    }
+  } else if constexpr (sizeof(T) == 4 && V == 4) {
+    const float4 r = *reinterpret_cast<const float4*>(src);
+    f[0] = r.x; f[1] = r.y; f[2] = r.z; f[3] = r.w;
   } else {
 #pragma unroll
     for (int e = 0; e < V; ++e) {
@@ -181,6 +206,121 @@ __global__ void __launch_bounds__(256) dwconv2d_nhwc(DwArgs a, unsigned long lon
   trace_end(trace);
 }
 
+// Shared-memory tiled variant (16-byte channel vectors, square 3/5/7 windows):
+// a CTA owns an 8 x 8 output tile x kCV channel vectors.  Its weights are
+// staged before griddepcontrol.wait (parameters), its input halo tile right
+// after with one coalesced 16-byte load per chunk (a single memory round trip
+// for the whole window), then every thread computes one output pixel-vector
+// from shared memory.
+constexpr int kTile = 8, kCV = 4;
+
+template <typename T, int V, int KS, int SS>
+__global__ void __launch_bounds__(kTile * kTile * kCV) dwconv2d_tiled(DwArgs a, unsigned long long* trace) {
+  constexpr int IH = (kTile - 1) * SS + KS, IW = IH;
+  constexpr int CW = kCV * V;   // channels per CTA
+  extern __shared__ __align__(16) uint8_t dsm[];
+  float* ws = reinterpret_cast<float*>(dsm);                       // [KS*KS][CW]
+  T* xs = reinterpret_cast<T*>(dsm + KS * KS * CW * sizeof(float));  // [IH][IW][CW]
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  const int tiles_w = (a.OW + kTile - 1) / kTile, tiles_h = (a.OH + kTile - 1) / kTile;
+  int bid = blockIdx.x;
+  const int tw = bid % tiles_w;
+  bid /= tiles_w;
+  const int th = bid % tiles_h;
+  bid /= tiles_h;
+  const int cgroups = (a.C + CW - 1) / CW;
+  const int cg = bid % cgroups;
+  const int b = bid / cgroups;
+  const int c0 = cg * CW;
+  // weights: KS*KS*kCV chunks of V fp32
+  for (int u = tid; u < KS * KS * kCV; u += blockDim.x) {
+    const int tap = u / kCV, cv = u % kCV, c = c0 + cv * V;
+    float w[V];
+    if (c < a.C) load_vec<float, V>(a.w + static_cast<int64_t>(tap) * a.C + c, w);
+    else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) w[e] = 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < V; ++e) ws[tap * CW + cv * V + e] = w[e];
+  }
+  pdl_wait();
+  trace_begin(trace);
+  const int ih0 = th * kTile * SS - a.ph, iw0 = tw * kTile * SS - a.pw;
+  const T* in = static_cast<const T*>(a.in) + static_cast<int64_t>(b) * a.H * a.W * a.in_cs + a.in_coff;
+  for (int u = tid; u < IH * IW * kCV; u += blockDim.x) {
+    const int cv = u % kCV, px = u / kCV, iy = px / IW, ix = px % IW;
+    const int ih = ih0 + iy, iw = iw0 + ix, c = c0 + cv * V;
+    float x[V];
+    if (ih >= 0 && ih < a.H && iw >= 0 && iw < a.W && c < a.C) {
+      load_vec<T, V>(in + (static_cast<int64_t>(ih) * a.W + iw) * a.in_cs + c, x);
+      if (a.relu_in) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) x[e] = fmaxf(x[e], 0.f);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) x[e] = 0.f;
+    }
+    store_vec<T, V>(xs + px * CW + cv * V, x);
+  }
+  __syncthreads();
+  const int cv = tid % kCV, p = tid / kCV, oy = p / kTile, ox = p % kTile;
+  const int oh = th * kTile + oy, ow = tw * kTile + ox, c = c0 + cv * V;
+  if (oh < a.OH && ow < a.OW && c < a.C) {
+    float acc[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] = 0.f;
+#pragma unroll
+    for (int r = 0; r < KS; ++r)
+#pragma unroll
+      for (int q = 0; q < KS; ++q) {
+        float x[V];
+        load_vec_plain<T, V>(xs + ((oy * SS + r) * IW + ox * SS + q) * CW + cv * V, x);
+        const float* w = ws + (r * KS + q) * CW + cv * V;
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = fmaf(x[e], w[e], acc[e]);
+      }
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const float v = acc[e] + (a.bias ? __ldg(a.bias + c + e) : 0.f);
+      acc[e] = a.act == 1 ? fmaxf(v, 0.f) : v;
+    }
+    store_vec<T, V>(static_cast<T*>(a.out) + ((static_cast<int64_t>(b) * a.OH + oh) * a.OW + ow) * a.out_cs +
+                        a.out_coff + c,
+                    acc);
+  }
+  trace_end(trace);
+}
+
+template <int KS, int SS>
+constexpr size_t tiled_smem(int v, int esz) {
+  return static_cast<size_t>(KS * KS * kCV * v) * 4 +
+         static_cast<size_t>(((kTile - 1) * SS + KS) * ((kTile - 1) * SS + KS) * kCV * v) * esz;
+}
+
+bool tiled_disabled() {
+  static const bool off = [] {
+    const char* v = std::getenv("OPARA_DW_TILED");
+    return v && v[0] == '0';
+  }();
+  return off;
+}
+
+template <typename T, int V>
+const void* pick_tiled(int ks, int ss, size_t* smem) {
+  constexpr int esz = sizeof(T);
+#define OPARA_DW_T(K, S)                                               \
+  if (ks == K && ss == S) {                                            \
+    *smem = tiled_smem<K, S>(V, esz);                                  \
+    return reinterpret_cast<const void*>(&dwconv2d_tiled<T, V, K, S>); \
+  }
+  OPARA_DW_T(3, 1) OPARA_DW_T(5, 1) OPARA_DW_T(7, 1) OPARA_DW_T(3, 2) OPARA_DW_T(5, 2) OPARA_DW_T(7, 2)
+#undef OPARA_DW_T
+  return nullptr;
+}
+
 template <typename T, int V>
 const void* pick_ks(int ks) {
   switch (ks) {
@@ -233,6 +373,25 @@ opara_status launch_dwconv2d(const opara_op& op, cudaStream_t s, unsigned long l
     vw = 2;
   const int ks = (a.kh == a.kw && (a.kh == 3 || a.kh == 5 || a.kh == 7)) ? a.kh : 0;
   LaunchCfg c;
+  // tiled shared-memory kernel for 16-byte vectors, square windows, equal strides 1/2
+  if (vw == V && ks && a.sh == a.sw && (a.sh == 1 || a.sh == 2) && !tiled_disabled()) {
+    size_t smem = 0;
+    c.func = bf ? pick_tiled<__nv_bfloat16, 8>(ks, a.sh, &smem) : pick_tiled<float, 4>(ks, a.sh, &smem);
+    if (c.func) {
+      const int cgroups = (a.C + kCV * V - 1) / (kCV * V);
+      c.block = dim3(kTile * kTile * kCV);
+      c.grid = dim3(static_cast<unsigned>(((a.OW + kTile - 1) / kTile) * ((a.OH + kTile - 1) / kTile) * cgroups * a.N));
+      c.smem = smem;
+      if (cfg) *cfg = c;
+      if (dry) return OPARA_OK;
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(c.func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return cuda_fail(e, "dwconv2d_tiled smem attribute");
+      }
+      void* args[] = {&a, &trace};
+      return launch_kernel(c, args, s);
+    }
+  }
   c.func = bf ? pick_dw<__nv_bfloat16>(vw, ks) : pick_dw<float>(vw, ks);
   const int64_t work = static_cast<int64_t>(a.N) * a.OH * ((a.OW + kPx - 1) / kPx) * (a.C / vw);
   c.block = dim3(256);   // (smaller CTAs on small maps measured slower)

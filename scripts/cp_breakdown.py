@@ -1,3 +1,5 @@
+import signal
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 """Critical-path breakdown of a profiled model (gpurun_out/profile_<tag>.json
 from scripts/profile_ops.py): per op kind, kernels and microseconds on the
 longest isolated-time path, plus totals over all ops."""
