@@ -430,6 +430,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     tc::cluster_sync();
   else
     __syncthreads();
+  // every TMEM read is done (the tile is in smem): free the columns now so a
+  // PDL-launched successor CTA on this SM can allocate while we reduce
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, kTmemCols);
+  }
   DBG(5);
   // rows [r0, r1) of the tile are reduced (over the cluster) and stored by this CTA
   const int rank = splits > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
@@ -484,11 +490,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   }
   DBG(6);
   if (splits > 1) tc::cluster_sync();  // peers may still be reading this CTA's tile
-  else __syncthreads();
-  if (warp == 0) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, kTmemCols);
-  }
   DBG(7);
   if (a.dbg && tid == 0 && cta_lin < 96) a.dbg[64 + 2 * cta_lin + 1] = global_ns();
 #undef DBG

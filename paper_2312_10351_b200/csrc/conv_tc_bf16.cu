@@ -396,6 +396,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     tc::cluster_sync();
   else
     __syncthreads();
+  // every TMEM read is done (the tile is in smem): free the columns now so a
+  // PDL-launched successor CTA on this SM can allocate while we reduce
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, kTmemCols);
+  }
   const int rank = splits > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
   const int rows_per = (BN + splits - 1) / splits;
   const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
@@ -456,12 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       }
     }
   }
-  if (splits > 1) tc::cluster_sync();
-  else __syncthreads();
-  if (warp == 0) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, kTmemCols);
-  }
+  if (splits > 1) tc::cluster_sync();  // peers may still be reading this CTA's tile
   trace_end(trace);
 }
 
