@@ -38,6 +38,11 @@ bool pdl_enabled() {
 }
 
 opara_status launch_kernel(const LaunchCfg& c, void** args, cudaStream_t s, unsigned cluster_z) {
+  return launch_kernel_cluster(c, args, s, dim3(1, 1, cluster_z));
+}
+
+opara_status launch_kernel_cluster(const LaunchCfg& c, void** args, cudaStream_t s, dim3 cluster) {
+  const unsigned cluster_z = cluster.x * cluster.y * cluster.z;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = c.grid;
   lc.blockDim = c.block;
@@ -52,9 +57,9 @@ opara_status launch_kernel(const LaunchCfg& c, void** args, cudaStream_t s, unsi
   }
   if (cluster_z > 1) {
     attr[n].id = cudaLaunchAttributeClusterDimension;
-    attr[n].val.clusterDim.x = 1;
-    attr[n].val.clusterDim.y = 1;
-    attr[n].val.clusterDim.z = cluster_z;
+    attr[n].val.clusterDim.x = cluster.x;
+    attr[n].val.clusterDim.y = cluster.y;
+    attr[n].val.clusterDim.z = cluster.z;
     ++n;
   }
   lc.attrs = attr;

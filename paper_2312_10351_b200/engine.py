@@ -316,6 +316,13 @@ class ScheduledGraph:
                 recs[k] = _op_record(op, self._views(op), self._weights(op),
                                      conv_engine_for(op, self.conv_engine), self.targets.get(k, 0),
                                      pull_of[k])
+                if op.kind == CONV2D and op.ints.get("ln"):   # fused residual + LayerNorm epilogue
+                    (rb, rcoff, rcs, _), = self._all_views(op)[1:2]
+                    arr = self._arrays(op)
+                    recs[k].i[27], recs[k].i[28] = 1, rcs
+                    recs[k].p[4] = _at(rb, rcoff, 2)
+                    recs[k].p[5], recs[k].p[6] = arr["gamma"], arr["beta"]
+                    recs[k].f[0] = op.floats[0]
         self.debug_ts = {}
         if os.environ.get("OPARA_CONV_DEBUG"):  # per-phase timestamps of CTA 0 (conv_tc.cu)
             for k, op in enumerate(program.ops):
@@ -426,7 +433,7 @@ class ScheduledGraph:
         L = _lib.lib()
         groups: dict[tuple, list[int]] = {}
         for k, op in enumerate(self.program.ops):
-            if op.kind == CONV2D and recs[k].i[22] in (1, 2):
+            if op.kind == CONV2D and recs[k].i[22] in (1, 2) and not recs[k].i[27]:
                 key = self._tune_key(recs[k]) + (self.targets.get(k, 0),)
                 groups.setdefault(key, []).append(k)
         cache_path = os.environ.get("OPARA_TUNE_CACHE")
@@ -641,7 +648,7 @@ class ScheduledGraph:
 
 
 def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "opara",
-            dtype: str = "f32",
+            dtype: str = "f32", fuse_layernorm: bool = False,
             gpu_config: GpuConfig | None = None, profile_reps: int = 20,
             seed: int | None = None, conv_engine: str = "tc",
             bound_grids: bool | str = False, tune: bool = True,
@@ -658,7 +665,7 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
     splitk: split-K reduction ("push" / "pull" / "auto", see ScheduledGraph) for
     a fixed grid policy; default pull with bounded grids, push with full grids."""
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-    program = lower(model, example, dtype)
+    program = lower(model, example, dtype, fuse_layernorm)
     if bound_grids != "auto":
         # measured default: pull reductions pair with bounded grids, push with full grids
         splitk = splitk or ("pull" if bound_grids else "push")
