@@ -353,6 +353,7 @@ def run_gpu(args) -> dict | None:
         "speedup_vs_sequential": round(t_seq.median_ms / lat_ms, 4),
         "grids": "bounded" if sg.bound_grids else "full",
         "splitk_reduction": sg.splitk,
+        "bound_scale": sg.bound_scale if sg.bound_grids else None,
         "grid_autotune": getattr(sg, "autotune", None),
         "sequential_best_latency_ms": round(min([t_seq.median_ms] + [a["sequential_ms"] for a in (
             getattr(sg, "autotune", None) or [])]), 4),

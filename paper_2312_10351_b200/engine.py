@@ -159,11 +159,13 @@ def concurrent_convs(program: Program) -> dict[int, int]:
     return {v: count[level[v]] for v, op in enumerate(program.ops) if op.kind == CONV2D}
 
 
-def concurrency_targets(program: Program, num_sms: int = 148) -> dict[int, int]:
+def concurrency_targets(program: Program, num_sms: int = 148, scale: float = 1.0) -> dict[int, int]:
     """CTA budget per conv: the SMs are shared among the convs of the same DAG
     level (longest-path depth) in proportion to their FLOPs, so branches that
     can run concurrently are sized to co-reside instead of each claiming the
-    whole GPU (Opara's bounded grids)."""
+    whole GPU (Opara's bounded grids).  `scale` oversubscribes
+    (> 1) or undersubscribes (< 1) the shares; compile(bound_grids="auto")
+    searches it."""
     level = dag_levels(program)
     work: dict[int, int] = {}
     for v, op in enumerate(program.ops):
@@ -172,7 +174,7 @@ def concurrency_targets(program: Program, num_sms: int = 148) -> dict[int, int]:
     out = {}
     for v, op in enumerate(program.ops):
         if op.kind == CONV2D and work.get(level[v]):
-            out[v] = max(8, int(round(num_sms * op.flops / work[level[v]])))
+            out[v] = max(8, int(round(scale * num_sms * op.flops / work[level[v]])))
     return out
 
 
@@ -289,7 +291,7 @@ class ScheduledGraph:
     def __init__(self, program: Program, device: int, policy: str = "opara",
                  gpu_config: GpuConfig | None = None, profile_reps: int = 20, seed: int | None = None,
                  conv_engine: str = "tc", bound_grids: bool = False, tune: bool = True,
-                 splitk: str = "push"):
+                 splitk: str = "push", bound_scale: float = 1.0):
         if not torch.cuda.is_available():
             raise RuntimeError("ScheduledGraph needs a CUDA device (there is no CPU fallback)")
         self.program = program
@@ -301,6 +303,7 @@ class ScheduledGraph:
         self._alloc(program)
         recs = (_lib.OparaOp * len(program.ops))()
         self.bound_grids = bool(bound_grids)
+        self.bound_scale = bound_scale
         # split-K reduction: "push" (st.async partials to the owner CTA), "pull" (DSMEM after a
         # cluster barrier), or "auto": pull where other convs share the DAG level (concurrent
         # branches), push for convs that run alone
@@ -308,7 +311,7 @@ class ScheduledGraph:
         conc = concurrent_convs(program) if splitk == "auto" else {}
         pull_of = {k: (splitk == "pull") or (splitk == "auto" and conc.get(k, 1) > 1)
                    for k in range(len(program.ops))}
-        self.targets = concurrency_targets(program) if bound_grids else {}
+        self.targets = concurrency_targets(program, scale=bound_scale) if bound_grids else {}
         for k, op in enumerate(program.ops):
             if op.kind in ROW_KINDS:
                 recs[k] = _op_record(op, self._all_views(op), self._arrays(op))
@@ -658,9 +661,9 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
     bound_grids: False = every conv/GEMM sized for the whole GPU; True =
     Opara's bounded grids (each conv sized for its DAG level's share of the
     SMs, so concurrent branches co-reside); "auto" = build every combination
-    of {full, bounded} grids x {push, pull, auto} split-K reductions, replay
-    each Opara graph and keep the fastest (all latencies are kept in
-    ``autotune`` for reporting).  tune: pick every tensor-core
+    of {full, bounded} grids x {push, pull, auto} split-K reductions (and,
+    when bounded wins, SM-share scales 0.75 / 1.5 / 2), replay each Opara
+    graph and keep the fastest (all latencies are kept in ``autotune``).  tune: pick every tensor-core
     conv/GEMM's tile width and split-K by measurement (ScheduledGraph._autotune).
     splitk: split-K reduction ("push" / "pull" / "auto", see ScheduledGraph) for
     a fixed grid policy; default pull with bounded grids, push with full grids."""
@@ -672,19 +675,29 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
         return ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine,
                               bool(bound_grids), tune, splitk)
     best, tried = None, []
+
+    def trial(bounded: bool, splitk: str, scale: float = 1.0):
+        nonlocal best
+        sg = ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine, bounded, tune,
+                            splitk, scale)
+        par = sg.time(SLOT_PARALLEL, warmup=5, iters=30).median_ms
+        seq = sg.time(SLOT_SEQUENTIAL, warmup=5, iters=30).median_ms
+        tried.append({"bounded": bounded, "splitk": splitk, "scale": scale, "parallel_ms": par,
+                      "sequential_ms": seq})
+        if best is None or par < best[1]:
+            if best is not None:
+                best[0].close()
+            best = (sg, par)
+        else:
+            sg.close()
+
     for bounded in (False, True):
         for splitk in ("push", "pull", "auto"):
-            sg = ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine, bounded, tune,
-                                splitk)
-            par = sg.time(SLOT_PARALLEL, warmup=5, iters=30).median_ms
-            seq = sg.time(SLOT_SEQUENTIAL, warmup=5, iters=30).median_ms
-            tried.append({"bounded": bounded, "splitk": splitk, "parallel_ms": par, "sequential_ms": seq})
-            if best is None or par < best[1]:
-                if best is not None:
-                    best[0].close()
-                best = (sg, par)
-            else:
-                sg.close()
+            trial(bounded, splitk)
+    if best[0].bound_grids:   # refine the SM shares of the winning bounded variant
+        splitk = best[0].splitk
+        for scale in (0.75, 1.5, 2.0):
+            trial(True, splitk, scale)
     sg = best[0]
     sg.autotune = tried
     return sg
