@@ -253,12 +253,11 @@ def run_gpu(args) -> dict | None:
     # engine's peak is the nominal fp32 FFMA rate (no measured figure exists).
     tc_peak_tflops = peaks["bf16_tflops"] / 2 / 3
     fam = {}
-    for op, p in zip(sg.program.ops, sg.profile):
+    for k, (op, p) in enumerate(zip(sg.program.ops, sg.profile)):
         if op.kind == 0:
             continue
         if op.kind == 1:
-            name = {0: "conv2d_f32_simt", 1: "conv2d_tc_tf32x3", 2: "conv2d_tc_bf16"}[
-                engine.conv_engine_for(op, sg.conv_engine)]
+            name = {0: "conv2d_f32_simt", 1: "conv2d_tc_tf32x3", 2: "conv2d_tc_bf16"}[sg.engines[k]]
         else:
             name = {2: "maxpool2d", 3: "avgpool2d", 4: "global_avgpool", 5: "linear_f32", 6: "add",
                     7: "layernorm", 9: "embedding", 10: "attention_tc", 11: "copy", 12: "fm", 13: "dwconv2d",
@@ -354,6 +353,8 @@ def run_gpu(args) -> dict | None:
         "grids": "bounded" if sg.bound_grids else "full",
         "splitk_reduction": sg.splitk,
         "bound_scale": sg.bound_scale if sg.bound_grids else None,
+        "conv_engines": {name: sum(1 for e in sg.engines.values() if e == code)
+                         for code, name in ((0, "simt_f32"), (1, "tc_tf32x3"), (2, "tc_bf16"))},
         "grid_autotune": getattr(sg, "autotune", None),
         "sequential_best_latency_ms": round(min([t_seq.median_ms] + [a["sequential_ms"] for a in (
             getattr(sg, "autotune", None) or [])]), 4),

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
       const int n = n0 + tx * TN + j;
       if (n < a.Cout) {
         float v = acc[i][j] + (a.bias ? __ldg(a.bias + n) : 0.f);
-        if (a.relu) v = fmaxf(v, 0.f);
+        if (a.relu) v = apply_act(v, a.relu);
         orow[n] = v;
       }
     }
@@ -285,7 +285,8 @@ opara_status launch_conv2d(const opara_op& op, cudaStream_t s, unsigned long lon
   a.OH = (int)op.i[6]; a.OW = (int)op.i[7]; a.Cout = (int)op.i[8];
   a.out_cs = (int)op.i[9]; a.out_coff = (int)op.i[10];
   a.R = (int)op.i[11]; a.S = (int)op.i[12]; a.sh = (int)op.i[13]; a.sw = (int)op.i[14];
-  a.ph = (int)op.i[15]; a.pw = (int)op.i[16]; a.relu = (int)op.i[17];
+  a.ph = (int)op.i[15]; a.pw = (int)op.i[16];
+  a.relu = conv_act_code(op.i[24], op.i[17]);   // `relu` carries the activation code
   a.relu_in = (int)op.i[25];
   if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "conv2d simt engine: fp32 only");
   a.M = a.N * a.OH * a.OW;

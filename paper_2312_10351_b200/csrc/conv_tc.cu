@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
         float y[4] = {acc.x + b, acc.y + b, acc.z + b, acc.w + b};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          if (a.relu) y[e] = fmaxf(y[e], 0.f);
+          y[e] = apply_act(y[e], a.relu);
           const int p = n0 + r0 + 4 * g + e;
           if (p < a.M) a.out[static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch] = y[e];
         }
@@ -475,8 +475,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     }
     acc.x += bias4.x; acc.y += bias4.y; acc.z += bias4.z; acc.w += bias4.w;
     if (a.relu) {
-      acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f);
-      acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
+      acc.x = apply_act(acc.x, a.relu); acc.y = apply_act(acc.y, a.relu);
+      acc.z = apply_act(acc.z, a.relu); acc.w = apply_act(acc.w, a.relu);
     }
     float* dst = a.out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
     if (a.vec_out && ch + 3 < a.Cout) {
@@ -629,7 +629,8 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   a.OH = (int)op.i[6]; a.OW = (int)op.i[7]; a.Cout = (int)op.i[8];
   a.out_cs = (int)op.i[9]; a.out_coff = (int)op.i[10];
   a.R = (int)op.i[11]; a.S = (int)op.i[12]; a.sh = (int)op.i[13]; a.sw = (int)op.i[14];
-  a.ph = (int)op.i[15]; a.pw = (int)op.i[16]; a.relu = (int)op.i[17];
+  a.ph = (int)op.i[15]; a.pw = (int)op.i[16];
+  a.relu = conv_act_code(op.i[24], op.i[17]);   // `relu` carries the activation code
   a.relu_in = (int)op.i[25];
   if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "conv2d tc engine: fp32 (3xTF32) only");
   a.M = a.N * a.OH * a.OW;

@@ -48,6 +48,20 @@ __device__ __forceinline__ bool splitk_arrive_last(unsigned* cnt, int splits) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Fused epilogue activation (opara_op CONV2D i[24]): 0 none, 1 ReLU, 2 GELU (erf), 3 tanh, 4 sigmoid.
+__device__ __forceinline__ float apply_act(float v, int act) {
+  switch (act) {
+    case 1: return fmaxf(v, 0.f);
+    case 2: return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+    case 3: return tanhf(v);
+    case 4: return 1.f / (1.f + expf(-v));
+    default: return v;
+  }
+}
+
+// Activation code of a CONV2D record: i[24] when set, else ReLU from i[17].
+inline int conv_act_code(long long act, long long relu) { return act ? static_cast<int>(act) : (relu ? 1 : 0); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

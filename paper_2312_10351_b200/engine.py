@@ -334,6 +334,7 @@ class ScheduledGraph:
                     self.debug_ts[k] = buf
                     recs[k].p[6] = buf.data_ptr()
         self.tuning = self._autotune(recs) if tune else {}
+        self.engines = {k: int(recs[k].i[22]) for k, op in enumerate(program.ops) if op.kind == CONV2D}
         self._recs = recs
         L = _lib.lib()
         h = C.c_void_p()
@@ -443,12 +444,36 @@ class ScheduledGraph:
         cache = {}
         if cache_path and Path(cache_path).exists():
             cache = {tuple(json.loads(k)): tuple(v) for k, v in json.loads(Path(cache_path).read_text()).items()}
+            cache = {k: ((tuple(v[0]),) + tuple(v[1:]) if isinstance(v[0], list) else v) for k, v in cache.items()}
         cands, owner, seen = [], [], set()
+        simt_w: dict[int, int] = {}   # op index -> device address of its unpacked [K][Cout] weights
         for key, ks in groups.items():
             if key in cache:
                 continue
             k0 = ks[0]
             budget = self.targets.get(k0, 0)
+            if recs[k0].i[22] == 1:
+                # fp32 convs may also run on the exact-FFMA SIMT engine (no TMEM / cluster
+                # overheads): let measurement decide per shape
+                t = torch.from_numpy(np.ascontiguousarray(self.program.ops[k0].weight)).to(self.dev)
+                self._keep.append(t)
+                simt_w[k0] = t.data_ptr()
+                for var in range(-1, 6):
+                    for sp in (1, 2, 4, 8, 16) if var >= 0 else (0,):
+                        rec = _lib.OparaOp()
+                        C.pointer(rec)[0] = recs[k0]
+                        rec.i[22], rec.p[1], rec.variant, rec.i[19] = 0, simt_w[k0], var, sp
+                        prof = _lib.OparaOpProfile()
+                        if L.opara_op_launch_config(C.byref(rec), C.byref(prof)) != 0:
+                            continue
+                        if budget and prof.num_blocks > max(budget, 8) * 2:
+                            continue
+                        launch = (key, "simt", prof.num_blocks, prof.threads_per_block)
+                        if launch in seen:
+                            continue
+                        seen.add(launch)
+                        cands.append(rec)
+                        owner.append((key, ("simt", var), sp, prof.num_blocks))
             for var in range(4):   # tile widths 32 << var (the 16-wide deep-ring tile hogs an SM: explicit only)
                 for sp in self.TUNE_SPLITS:
                     rec = _lib.OparaOp()
@@ -477,7 +502,7 @@ class ScheduledGraph:
                 L.opara_exec_destroy(h)
             for (key, var, sp, _), p in zip(owner, out):
                 if key not in best or p.isolated_us < best[key][2]:
-                    best[key] = (var, sp, p.isolated_us)
+                    best[key] = (var, sp, p.isolated_us)   # var: tile id, or ("simt", SIMT variant)
             if cache_path:   # persist: later compiles of the same shapes skip the search
                 cache.update(best)
                 Path(cache_path).write_text(json.dumps({json.dumps(list(k)): list(v) for k, v in cache.items()}))
@@ -486,7 +511,15 @@ class ScheduledGraph:
             if key in best:
                 var, sp, us = best[key]
                 for k in ks:
-                    recs[k].variant, recs[k].i[19] = var, sp
+                    if isinstance(var, (tuple, list)):   # ("simt", variant): switch engine + weights
+                        if k not in simt_w:
+                            t = torch.from_numpy(np.ascontiguousarray(self.program.ops[k].weight)).to(self.dev)
+                            self._keep.append(t)
+                            simt_w[k] = t.data_ptr()
+                        recs[k].i[22], recs[k].p[1] = 0, simt_w[k]
+                        recs[k].variant, recs[k].i[19] = var[1], sp
+                    else:
+                        recs[k].variant, recs[k].i[19] = var, sp
                     chosen[k] = (var, sp, us)
         return chosen
 
