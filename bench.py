@@ -169,6 +169,13 @@ def workload_name(args, x) -> str:
     return f"{args.model} batch={args.batch} {args.dtype} ({shape})"
 
 
+def broadcast_value(dist, rank: int, compute):
+    """compute() on rank 0, its (picklable) result on every rank."""
+    box = [compute() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
 def run_gpu(args) -> dict | None:
     import torch
     import torch.distributed as dist
@@ -185,8 +192,25 @@ def run_gpu(args) -> dict | None:
 
     model, ref_model, x = build_workload(args)
     bound = {"auto": "auto", "bounded": True, "full": False}[args.grids]
-    sg = engine.compile(model, x, device=local, bound_grids=bound, profile_reps=args.profile_reps,
-                        dtype=args.dtype)
+    if world > 1 and bound == "auto":
+        # replicas run identical graphs: rank 0 searches the sizing variants and
+        # tiles once, the other ranks compile its choice from the shared tuning cache
+        import tempfile
+        os.environ["OPARA_TUNE_CACHE"] = broadcast_value(dist, rank, lambda: os.environ.get("OPARA_TUNE_CACHE") or
+                                                         os.path.join(tempfile.gettempdir(),
+                                                                      f"opara_tune_{os.getpid()}.json"))
+        sg = None
+        if rank == 0:
+            sg = engine.compile(model, x, device=local, bound_grids="auto", profile_reps=args.profile_reps,
+                                dtype=args.dtype)
+        bounded, splitk, scale = broadcast_value(dist, rank, lambda: (sg.bound_grids, sg.splitk, sg.bound_scale))
+        if rank != 0:
+            program = engine.lower(model, x, args.dtype)
+            sg = engine.ScheduledGraph(program, local, profile_reps=args.profile_reps, bound_grids=bounded,
+                                       splitk=splitk, bound_scale=scale)
+    else:
+        sg = engine.compile(model, x, device=local, bound_grids=bound, profile_reps=args.profile_reps,
+                            dtype=args.dtype)
     xd = tuple(t.cuda(local) for t in x) if isinstance(x, tuple) else x.cuda(local)
     # correctness guard on every rank: a fast wrong answer is not a result
     y = sg.run(xd)

@@ -31,7 +31,10 @@ def _worker(rank, world, port, q):
     order = op.order_opara(g, op.GPU_PRESETS["b200"]).order
     fake_seconds = torch.tensor([1.0 + rank], dtype=torch.float64)
     dist.all_reduce(fake_seconds, op=dist.ReduceOp.MAX)
-    q.put((rank, plan.num_streams, hash(order), float(fake_seconds)))
+    # bench.py: rank 0 picks the sizing variant, every replica compiles the same one
+    import bench
+    choice = bench.broadcast_value(dist, rank, lambda: (True, "pull", 1.5) if rank == 0 else None)
+    q.put((rank, plan.num_streams, hash(order), float(fake_seconds), choice))
     dist.destroy_process_group()
 
 
@@ -47,3 +50,4 @@ def test_two_replicas_schedule_identically_and_time_is_max():
         p.join(timeout=60)
     assert res[0][1:3] == res[1][1:3] == (28, res[0][2])
     assert res[0][3] == res[1][3] == 2.0
+    assert res[0][4] == res[1][4] == (True, "pull", 1.5)
