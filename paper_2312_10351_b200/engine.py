@@ -713,8 +713,8 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
         nonlocal best
         sg = ScheduledGraph(program, device, policy, gpu_config, profile_reps, seed, conv_engine, bounded, tune,
                             splitk, scale)
-        par = sg.time(SLOT_PARALLEL, warmup=5, iters=30).median_ms
-        seq = sg.time(SLOT_SEQUENTIAL, warmup=5, iters=30).median_ms
+        par = sg.time(SLOT_PARALLEL, warmup=10, iters=100).median_ms
+        seq = sg.time(SLOT_SEQUENTIAL, warmup=10, iters=60).median_ms
         tried.append({"bounded": bounded, "splitk": splitk, "scale": scale, "parallel_ms": par,
                       "sequential_ms": seq})
         if best is None or par < best[1]:
