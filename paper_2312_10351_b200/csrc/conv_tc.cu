@@ -496,6 +496,243 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   trace_end(trace);
 }
 
+// ---------------------------------------------------------------------------
+// Pixel-major variant for narrow convolutions (Cout <= NW = 32 / 64): the
+// output pixels sit on UMMA M (128 per CTA) and the channels on N = NW, so a
+// 32-channel stem conv does not pad its weights to 128 MMA rows (4x wasted
+// tensor work in the channel-major kernel above).  Same producer structure
+// (cp.async im2col into the 64-byte-swizzled X planes, convert warps for the
+// tf32 lo plane, bulk-copied host-packed W hi/lo planes of NW rows, one MMA
+// lane issuing 3 tcgen05.mma per 8-wide k step); no split-K (narrow layers
+// are pixel-rich).  Epilogue: thread = pixel row (TMEM lane), its NW channel
+// columns summed over the three accumulators, bias + activation, stored as
+// 16-byte vectors of the pixel's output row.
+constexpr int kPxStages = 4;
+
+template <int NW, bool kVec>
+__global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3_px(TcArgs a, unsigned long long* trace) {
+  constexpr int BM = 128;                           // pixels per CTA (UMMA M)
+  constexpr uint32_t kWB = NW * kBKF * 4;           // one W plane per stage
+  constexpr uint32_t kXB = BM * kBKF * 4;           // one X plane per stage
+  constexpr uint32_t kStage = 2 * kWB + 2 * kXB;
+  constexpr uint32_t kSbo = 512;
+  constexpr int kRowGroups = BM / 8;
+  constexpr int kRowsPerThread = kRowGroups / 4;
+  constexpr uint32_t kIdesc = tc::instr_desc(2, 128, NW);
+  constexpr uint32_t kTmemCols = 3 * NW <= 128 ? 128 : 256;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPxStages * kStage);
+  uint64_t* empty = full + kPxStages;
+  uint64_t* landed = empty + kPxStages;
+  uint64_t* accum = landed + kPxStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(accum + 1);
+  float* bias_s = reinterpret_cast<float*>(accum + 2);   // NW fp32
+
+  pdl_trigger();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n0 = blockIdx.x * BM;
+  const int nkb = a.kblocks;
+  if (tid < NW) bias_s[tid] = (a.bias && tid < a.Cout) ? __ldg(a.bias + tid) : 0.f;   // parameter: pre-wait
+  if (tid == 0) {
+    for (int st = 0; st < kPxStages; ++st) {
+      tc::mbar_init(&full[st], 32 * (kProducerWarps / 2) + 1);
+      tc::mbar_init(&landed[st], 32 * (kProducerWarps / 2));
+      tc::mbar_init(&empty[st], 1);
+    }
+    tc::mbar_init(accum, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, kTmemCols);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp < kProducerWarps) {
+    const bool gather = warp < kProducerWarps / 2;
+    const int rw = warp & 3;
+    const int r8 = lane & 7, cl = lane >> 3;
+    auto x_off = [&](int j) -> uint32_t {
+      return static_cast<uint32_t>(rw + 4 * j) * kSbo + r8 * 64u + static_cast<uint32_t>((cl ^ ((r8 >> 1) & 3)) * 16);
+    };
+    if (gather) {
+      int pb[kRowsPerThread], pih[kRowsPerThread], piw[kRowsPerThread];
+      const int ohw = a.OH * a.OW;
+#pragma unroll
+      for (int j = 0; j < kRowsPerThread; ++j) {
+        const int p = n0 + (rw + 4 * j) * 8 + r8;
+        if (p < a.M) {
+          const int b = p / ohw, rem = p - b * ohw, oh = rem / a.OW, ow = rem - oh * a.OW;
+          pb[j] = b;
+          pih[j] = oh * a.sh - a.ph;
+          piw[j] = ow * a.sw - a.pw;
+        } else {
+          pb[j] = -1;
+          pih[j] = 0;
+          piw[j] = 0;
+        }
+      }
+      const float* rowbase[kRowsPerThread];
+#pragma unroll
+      for (int j = 0; j < kRowsPerThread; ++j)
+        rowbase[j] = a.in + (pb[j] >= 0 ? pb[j] * a.sN + pih[j] * a.sH + piw[j] * a.sW + a.in_coff : 0);
+      int kc = cl * 4, dc = 0, dr = 0, dq = 0;
+      if (kVec && kc < a.K) {
+        dc = kc % a.Cin;
+        const int rs = kc / a.Cin;
+        dr = rs / a.S;
+        dq = rs - dr * a.S;
+      }
+      pdl_wait();
+      trace_begin(trace);
+      for (int i = 0; i < nkb; ++i) {
+        const int st = i % kPxStages;
+        if (i >= kPxStages) tc::mbar_wait(&empty[st], ((i / kPxStages) - 1) & 1);
+        const uint32_t xh = tc::smem_u32(smem + st * kStage + 2 * kWB);
+        if constexpr (kVec) {
+          const bool kin = kc < a.K;
+          const int64_t koff = dr * a.sH + dq * a.sW + dc;
+#pragma unroll
+          for (int j = 0; j < kRowsPerThread; ++j) {
+            const int ih = pih[j] + dr, iw = piw[j] + dq;
+            const bool ok = kin && pb[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+            cp_async16(xh + x_off(j), ok ? rowbase[j] + koff : a.in, ok);
+          }
+          kc += kBKF;
+          dc += kBKF;
+          while (dc >= a.Cin) {
+            dc -= a.Cin;
+            if (++dq == a.S) {
+              dq = 0;
+              ++dr;
+            }
+          }
+        } else {
+          const int kbase = i * kBKF + cl * 4;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = kbase + e;
+            const bool kin = k < a.K;
+            int c = 0, r = 0, q = 0;
+            if (kin) {
+              c = k % a.Cin;
+              const int rs = k / a.Cin;
+              r = rs / a.S;
+              q = rs - r * a.S;
+            }
+#pragma unroll
+            for (int j = 0; j < kRowsPerThread; ++j) {
+              const int ih = pih[j] + r, iw = piw[j] + q;
+              const bool ok = kin && pb[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+              const float* src = ok ? a.in + pb[j] * a.sN + ih * a.sH + iw * a.sW + c * a.sC + a.in_coff : a.in;
+              cp_async4(xh + x_off(j) + 4 * e, src, ok);
+            }
+          }
+        }
+        tc::cp_async_arrive_noinc(&landed[st]);
+      }
+    } else {
+      for (int i = 0; i < nkb; ++i) {
+        const int st = i % kPxStages;
+        tc::mbar_wait(&landed[st], (i / kPxStages) & 1);
+        uint8_t* xh = smem + st * kStage + 2 * kWB;
+        uint8_t* xl = xh + kXB;
+#pragma unroll
+        for (int j = 0; j < kRowsPerThread; ++j) {
+          float4 v = *reinterpret_cast<const float4*>(xh + x_off(j));
+          if (a.relu_in) {
+            v.x = fmaxf(v.x, 0.f);
+            v.y = fmaxf(v.y, 0.f);
+            v.z = fmaxf(v.z, 0.f);
+            v.w = fmaxf(v.w, 0.f);
+            *reinterpret_cast<float4*>(xh + x_off(j)) = v;
+          }
+          float4 lo;
+          lo.x = v.x - tc::trunc_tf32(v.x);
+          lo.y = v.y - tc::trunc_tf32(v.y);
+          lo.z = v.z - tc::trunc_tf32(v.z);
+          lo.w = v.w - tc::trunc_tf32(v.w);
+          *reinterpret_cast<float4*>(xl + x_off(j)) = lo;
+        }
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&full[st]);
+      }
+    }
+  } else if (warp == kLoadWarp) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int st = i % kPxStages;
+        if (i >= kPxStages) tc::mbar_wait(&empty[st], ((i / kPxStages) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&full[st], 2 * kWB);
+        tc::bulk_g2s(smem + st * kStage, a.wpack + static_cast<int64_t>(i) * (2 * kWB / 4), 2 * kWB, &full[st]);
+      }
+    }
+  } else if (lane == 0) {
+    for (int i = 0; i < nkb; ++i) {
+      const int st = i % kPxStages;
+      tc::mbar_wait(&full[st], (i / kPxStages) & 1);
+      tc::tc_fence_after();
+      const uint32_t base = tc::smem_u32(smem + st * kStage);
+      const uint32_t w_hi = base, w_lo = base + kWB, x_hi = base + 2 * kWB, x_lo = x_hi + kXB;
+#pragma unroll
+      for (int ks = 0; ks < kBKF / 8; ++ks) {
+        const uint64_t ah = tc::smem_desc_sw64(x_hi + 32 * ks, kSbo);   // A = X (pixels on M)
+        const uint64_t al = tc::smem_desc_sw64(x_lo + 32 * ks, kSbo);
+        const uint64_t bh = tc::smem_desc_sw64(w_hi + 32 * ks, kSbo);   // B = W (channels on N)
+        const uint64_t bl = tc::smem_desc_sw64(w_lo + 32 * ks, kSbo);
+        const uint32_t acc = (i | ks) != 0;
+        tc::mma_tf32(tmem, ah, bh, kIdesc, acc);
+        tc::mma_tf32(tmem + NW, ah, bl, kIdesc, acc);
+        tc::mma_tf32(tmem + 2 * NW, al, bh, kIdesc, acc);
+      }
+      tc::mma_commit(&empty[st]);
+    }
+    tc::mma_commit(accum);
+  }
+  __syncwarp();
+
+  if (warp < 4) {
+    tc::mbar_wait(accum, 0);
+    tc::tc_fence_after();
+    const int p = n0 + warp * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    float* orow = a.out + static_cast<int64_t>(p) * a.out_cs + a.out_coff;
+#pragma unroll
+    for (int c8 = 0; c8 < NW / 8; ++c8) {
+      float v[8], v1[8], v2[8];
+      tc::tmem_ld8(trow + c8 * 8, v);
+      tc::tmem_ld8(trow + NW + c8 * 8, v1);
+      tc::tmem_ld8(trow + 2 * NW + c8 * 8, v2);
+      if (p < a.M) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = apply_act(v[e] + (v1[e] + v2[e]) + bias_s[c8 * 8 + e], a.relu);
+        const int c0 = c8 * 8;
+        if (a.vec_out && c0 + 7 < a.Cout) {
+          *reinterpret_cast<float4*>(orow + c0) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4*>(orow + c0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (c0 + e < a.Cout) orow[c0 + e] = v[e];
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, kTmemCols);
+  }
+  trace_end(trace);
+}
+
+template <int NW>
+constexpr size_t tc_px_smem_bytes() {
+  return kPxStages * (2 * static_cast<size_t>(NW) * kBKF * 4 + 2 * 128 * kBKF * 4) + 512 + 1024;
+}
+
 template <int BN>
 constexpr size_t tc_smem_bytes() {
   return tc_stages(BN) * (2 * kWBytes + 2 * static_cast<size_t>(BN) * kBKF * 4) + 512 + 1024;
@@ -653,6 +890,37 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   const bool vec = !nchw && a.Cin % 4 == 0 && in_cs % 4 == 0 && a.in_coff % 4 == 0 &&
                    reinterpret_cast<uintptr_t>(a.in) % 16 == 0;
   a.vec_out = (a.out_cs % 4 == 0 && a.out_coff % 4 == 0 && reinterpret_cast<uintptr_t>(a.out) % 16 == 0) ? 1 : 0;
+  if (op.variant == 4 || op.variant == 5) {
+    // pixel-major tile for narrow convs: p[1] holds W packed with NW rows
+    // (engine.pack_conv_weights_tf32x3(w, rows=NW)); no split-K
+    const int nw = op.variant == 4 ? 32 : 64;
+    if (a.Cout > nw) return fail(OPARA_ERR_VALUE, "conv2d_tc pixel-major tile: Cout exceeds the tile width");
+    a.splits = 1;
+    a.kb_per_split = a.kblocks;
+    a.push = 0;
+    LaunchCfg c;
+    c.func = nw == 32 ? (vec ? reinterpret_cast<const void*>(&conv2d_tc_tf32x3_px<32, true>)
+                             : reinterpret_cast<const void*>(&conv2d_tc_tf32x3_px<32, false>))
+                      : (vec ? reinterpret_cast<const void*>(&conv2d_tc_tf32x3_px<64, true>)
+                             : reinterpret_cast<const void*>(&conv2d_tc_tf32x3_px<64, false>));
+    c.grid = dim3(ceil_div(a.M, 128), 1, 1);
+    c.block = dim3(kThreads);
+    c.smem = nw == 32 ? tc_px_smem_bytes<32>() : tc_px_smem_bytes<64>();
+    if (cfg) *cfg = c;
+    if (dry) return OPARA_OK;
+    static std::mutex mu;
+    static std::map<const void*, bool> done;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (!done[c.func]) {
+        cudaError_t e = cudaFuncSetAttribute(c.func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
+        if (e != cudaSuccess) return cuda_fail(e, "conv2d_tc_px smem attribute");
+        done[c.func] = true;
+      }
+    }
+    void* args[] = {&a, &trace};
+    return launch_kernel(c, args, s);
+  }
   int count = 0;
   const TcVariant* v = tc_variants(&count);
   int id = 0, splits = 1;

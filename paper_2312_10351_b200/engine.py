@@ -109,18 +109,20 @@ def tf32_rna(x: np.ndarray) -> np.ndarray:
     return b.view(np.float32)
 
 
-def pack_conv_weights_tf32x3(wk: np.ndarray) -> np.ndarray:
+def pack_conv_weights_tf32x3(wk: np.ndarray, rows: int = 128) -> np.ndarray:
     """[K][Cout] fp32 conv weights -> the tcgen05 engine's W operand images.
 
-    Rows = output channels (UMMA M, padded to 128-row tiles), columns = k
-    (padded to 16-element blocks).  Every (m-tile, k-block) becomes one
-    contiguous 16 KiB record: the tf32 hi plane then the tf32 lo plane, each in
-    the 64-byte-swizzled K-major order [atom(16)][row(8)][chunk(4), XOR-permuted
-    by (row >> 1) & 3][4 fp32] that conv_tc.cu's SWIZZLE_64B descriptors expect.
+    Rows = output channels (UMMA M in 128-row tiles; or, for the pixel-major
+    narrow-conv tile, UMMA N = `rows` = 32 / 64), columns = k (padded to
+    16-element blocks).  Every (row-tile, k-block) becomes one contiguous
+    record: the tf32 hi plane then the tf32 lo plane, each in the
+    64-byte-swizzled K-major order [atom(rows/8)][row(8)][chunk(4),
+    XOR-permuted by (row >> 1) & 3][4 fp32] that conv_tc.cu's SWIZZLE_64B
+    descriptors expect.
     """
     k, cout = wk.shape
-    mt, kb = -(-cout // 128), -(-k // 16)
-    w = np.zeros((mt * 128, kb * 16), dtype=np.float32)
+    mt, kb = -(-cout // rows), -(-k // 16)
+    w = np.zeros((mt * rows, kb * 16), dtype=np.float32)
     w[:cout, :k] = wk.T
     hi = tf32_rna(w)
     lo = tf32_rna(w - hi)  # hi/lo exact tf32 values: the hardware truncation is a no-op on them
@@ -132,7 +134,7 @@ def pack_conv_weights_tf32x3(wk: np.ndarray) -> np.ndarray:
     inv = np.argsort(perm, axis=1)     # source chunk stored at destination chunk
 
     def image(x):
-        t = x.reshape(mt, 16, 8, kb, 4, 4).transpose(0, 3, 1, 2, 4, 5)  # (mt, kb, atom, r, chunk, e)
+        t = x.reshape(mt, rows // 8, 8, kb, 4, 4).transpose(0, 3, 1, 2, 4, 5)  # (mt, kb, atom, r, chunk, e)
         return np.take_along_axis(t, inv[None, None, None, :, :, None], axis=4)
 
     return np.ascontiguousarray(np.stack([image(hi), image(lo)], axis=2)).reshape(-1)
@@ -447,6 +449,7 @@ class ScheduledGraph:
             cache = {k: ((tuple(v[0]),) + tuple(v[1:]) if isinstance(v[0], list) else v) for k, v in cache.items()}
         cands, owner, seen = [], [], set()
         simt_w: dict[int, int] = {}   # op index -> device address of its unpacked [K][Cout] weights
+        px_w: dict[tuple, int] = {}   # (op index, variant) -> pixel-major packed weights
         for key, ks in groups.items():
             if key in cache:
                 continue
@@ -474,6 +477,22 @@ class ScheduledGraph:
                         seen.add(launch)
                         cands.append(rec)
                         owner.append((key, ("simt", var), sp, prof.num_blocks))
+                # narrow convs: the pixel-major tile (pixels on UMMA M, channels on N)
+                cout = self.program.ops[k0].ints["Cout"]
+                for var, nw in ((4, 32), (5, 64)):
+                    if cout > nw:
+                        continue
+                    t = torch.from_numpy(pack_conv_weights_tf32x3(self.program.ops[k0].weight, rows=nw)).to(self.dev)
+                    self._keep.append(t)
+                    px_w[(k0, var)] = t.data_ptr()
+                    rec = _lib.OparaOp()
+                    C.pointer(rec)[0] = recs[k0]
+                    rec.p[1], rec.variant, rec.i[19] = px_w[(k0, var)], var, 0
+                    prof = _lib.OparaOpProfile()
+                    if L.opara_op_launch_config(C.byref(rec), C.byref(prof)) != 0:
+                        continue
+                    cands.append(rec)
+                    owner.append((key, ("px", var), 0, prof.num_blocks))
             for var in range(4):   # tile widths 32 << var (the 16-wide deep-ring tile hogs an SM: explicit only)
                 for sp in self.TUNE_SPLITS:
                     rec = _lib.OparaOp()
@@ -511,13 +530,20 @@ class ScheduledGraph:
             if key in best:
                 var, sp, us = best[key]
                 for k in ks:
-                    if isinstance(var, (tuple, list)):   # ("simt", variant): switch engine + weights
+                    if isinstance(var, (tuple, list)) and var[0] == "simt":   # switch engine + weights
                         if k not in simt_w:
                             t = torch.from_numpy(np.ascontiguousarray(self.program.ops[k].weight)).to(self.dev)
                             self._keep.append(t)
                             simt_w[k] = t.data_ptr()
                         recs[k].i[22], recs[k].p[1] = 0, simt_w[k]
                         recs[k].variant, recs[k].i[19] = var[1], sp
+                    elif isinstance(var, (tuple, list)):   # ("px", variant): pixel-major packed weights
+                        if (k, var[1]) not in px_w:
+                            t = torch.from_numpy(pack_conv_weights_tf32x3(self.program.ops[k].weight,
+                                                                          rows=32 if var[1] == 4 else 64)).to(self.dev)
+                            self._keep.append(t)
+                            px_w[(k, var[1])] = t.data_ptr()
+                        recs[k].p[1], recs[k].variant, recs[k].i[19] = px_w[(k, var[1])], var[1], 0
                     else:
                         recs[k].variant, recs[k].i[19] = var, sp
                     chosen[k] = (var, sp, us)

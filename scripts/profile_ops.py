@@ -25,7 +25,7 @@ sg.run(tuple(t.cuda() for t in x) if isinstance(x, tuple) else x.cuda())
 rows = []
 for k, (op, p) in enumerate(zip(sg.program.ops, sg.profile)):
     rows.append({"id": k + 1, "kind": op.kind, "label": op.label, "ints": op.ints, "flops": op.flops,
-                 "bytes": op.bytes_min, **p})
+                 "bytes": op.bytes_min, "engine": sg.engines.get(k), "tuning": sg.tuning.get(k), **p})
 out = {"model": args.model, "dtype": args.dtype, "grids": "bounded" if sg.bound_grids else "full", "ops": rows,
        "edges": sg.program.edges, "trace_parallel": sg.trace(engine.SLOT_PARALLEL),
        "trace_sequential": sg.trace(engine.SLOT_SEQUENTIAL), "order": list(sg.schedule.order),

@@ -132,3 +132,44 @@ def test_deepfm_parity(batch):
         ref = model.cuda()(dense.cuda(), ids.cuda())
     assert _rel(y, ref) <= 1e-5
     assert sg.plan.num_streams > 20  # the per-field gathers run as parallel branches
+
+
+@pytest.mark.parametrize("cin,cout,k,s,hw", [(32, 32, 3, 1, 37), (64, 48, 1, 1, 29), (16, 64, 3, 2, 41),
+                                           (192, 32, 5, 1, 17)])
+def test_pixel_major_tf32x3_tile(cin, cout, k, s, hw):
+    """The pixel-major 3xTF32 tile (pixels on UMMA M, <= 64 channels on N,
+    variant 4/5 with its own weight packing) against the fp32 reference."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2312_10351_b200 import _lib, engine
+    torch.manual_seed(2)
+    conv = nn.Conv2d(cin, cout, k, s, k // 2, bias=False)
+    bn = _bn(cout)
+    stem = nn.Conv2d(3, cin, 1, bias=False)
+    m = nn.Sequential(stem, nn.ReLU(), conv, bn, nn.ReLU()).eval()
+    x = torch.randn(1, 3, hw, hw)
+    sg = engine.ScheduledGraph(engine.lower(m, x, "f32"), 0, profile_reps=1, tune=False)
+    k_conv = max(i for i, op in enumerate(sg.program.ops) if op.kind == 1)
+    op = sg.program.ops[k_conv]
+    var, nw = (4, 32) if cout <= 32 else (5, 64)
+    wpx = torch.from_numpy(engine.pack_conv_weights_tf32x3(op.weight, rows=nw)).cuda()
+    recs = (_lib.OparaOp * len(sg._recs))()
+    C.memmove(recs, sg._recs, C.sizeof(sg._recs))
+    recs[k_conv].variant, recs[k_conv].p[1], recs[k_conv].i[19], recs[k_conv].i[22] = var, wpx.data_ptr(), 0, 1
+    L = _lib.lib()
+    h = C.c_void_p()
+    _lib.check(L.opara_exec_create(0, C.cast(recs, C.c_void_p), len(recs), C.byref(h)))
+    try:
+        sg.input_buffer.copy_(x.cuda())
+        order = np.asarray(range(len(recs)), dtype=np.int64)
+        _lib.check(L.opara_exec_run_eager(h, _lib.ptr(order), len(order),
+                                          C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        torch.cuda.synchronize()
+        y = sg.output_buffer.clone()
+    finally:
+        L.opara_exec_destroy(h)
+    with torch.no_grad():   # float64 on the CPU: cuDNN may pick Winograd / FFT for 5x5 (~1e-4 error)
+        ref = m.double()(x.double()).permute(0, 2, 3, 1)
+    assert _rel(y.cpu().reshape(ref.shape), ref) <= 1e-5
