@@ -252,6 +252,14 @@ def run_gpu(args) -> dict | None:
     t_seq_warm = sg.time(engine.SLOT_SEQUENTIAL, warmup=args.warmup, iters=args.steps, flush_l2=False)
     step_total_s = sum(t_par.samples) / 1e3
 
+    # launch-order sensitivity (the paper's Fig. 2 question): the same kernels and
+    # Alg. 1 plan captured with the baseline orders, timed like the Opara graph
+    orders = {}
+    from paper_2312_10351_b200.order import make_order
+    for slot, pol in ((10, "dfs"), (11, "wavefront")):
+        sg.capture(slot, sg.plan, make_order(sg.graph, pol, sg.gpu_config))
+        orders[pol] = round(sg.time(slot, warmup=args.warmup, iters=args.steps, flush_l2=True).median_ms, 4)
+
     # e2e through the public API: pinned host in -> H2D -> replay -> D2H logits
     e2e = sg.time_host_roundtrip(x, warmup=args.warmup, iters=args.steps)
 
@@ -385,6 +393,8 @@ def run_gpu(args) -> dict | None:
         "latency_warm_l2_ms": round(t_warm.median_ms, 4),
         "sequential_latency_warm_l2_ms": round(t_seq_warm.median_ms, 4),
         "speedup_vs_sequential_warm_l2": round(t_seq_warm.median_ms / t_warm.median_ms, 4),
+        "launch_order_latency_ms": {"opara": round(lat_ms, 4), **orders,
+                                    "sequential": round(t_seq.median_ms, 4)},
         "speedup_vs_best_sequential": round(min([t_seq.median_ms] + [a["sequential_ms"] for a in (
             getattr(sg, "autotune", None) or [])]) / lat_ms, 4),
         "dag_roofline": {"critical_path_us": round(cp_us, 2), "flop_term_us": round(flop_term_us, 2),
