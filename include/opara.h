@@ -230,6 +230,10 @@ opara_status opara_exec_capture(opara_exec* ex, int32_t slot, const int32_t* str
                                 int64_t n_sync);
 /* Replay the graph in `slot` on a caller stream (cudaStream_t as void*; NULL =
  * the legacy default stream).  Asynchronous. */
+/* Per-op CUDA scheduling priority for graphs captured afterwards (NULL clears):
+ * lower = more urgent, clamped to cudaDeviceGetStreamPriorityRange; captured
+ * graphs are instantiated with cudaGraphInstantiateFlagUseNodePriority. */
+opara_status opara_exec_set_priorities(opara_exec* ex, const int32_t* prio);
 opara_status opara_exec_replay(opara_exec* ex, int32_t slot, void* stream);
 /* Launch every op eagerly in `order` on one stream (debugging / profiling). */
 opara_status opara_exec_run_eager(opara_exec* ex, const int64_t* order, int64_t n, void* stream);

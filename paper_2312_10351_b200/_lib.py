@@ -98,6 +98,7 @@ SIGNATURES = {
     "opara_exec_create": (C.c_int, [C.c_int32, _P, C.c_int64, C.POINTER(_P)]),
     "opara_exec_destroy": (None, [_P]),
     "opara_exec_capture": (C.c_int, [_P, C.c_int32, _P, C.c_int32, _P, _P, C.c_int64]),
+    "opara_exec_set_priorities": (C.c_int, [_P, _P]),
     "opara_exec_replay": (C.c_int, [_P, C.c_int32, _P]),
     "opara_exec_run_eager": (C.c_int, [_P, _P, C.c_int64, _P]),
     "opara_exec_profile": (C.c_int, [_P, C.c_int32, _P]),

@@ -29,6 +29,10 @@ opara_status cuda_fail(cudaError_t e, const char* what) {
                                   cudaGetErrorString(e) + ")");
 }
 
+// Per-launch scheduling priority applied by launch_kernel (0 = default); the
+// capture sets it per op from opara_exec_set_priorities.
+thread_local int g_launch_priority = 0;
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("OPARA_PDL");
@@ -48,8 +52,13 @@ opara_status launch_kernel_cluster(const LaunchCfg& c, void** args, cudaStream_t
   lc.blockDim = c.block;
   lc.dynamicSmemBytes = c.smem;
   lc.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   unsigned n = 0;
+  if (g_launch_priority != 0) {
+    attr[n].id = cudaLaunchAttributePriority;
+    attr[n].val.priority = g_launch_priority;
+    ++n;
+  }
   if (pdl_enabled()) {
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n].val.programmaticStreamSerializationAllowed = 1;
@@ -119,6 +128,7 @@ struct opara_exec {
   };
   int32_t device = 0;
   std::vector<opara_op> ops;
+  std::vector<int32_t> prio;   // per-op CUDA priority for captured graphs (empty = none)
   std::map<int32_t, Plan> plans;
   std::map<int32_t, Graph> graphs;         // plain replay graphs
   std::map<int32_t, Graph> traced_graphs;  // same plan, kernels write timestamps
@@ -252,7 +262,9 @@ opara_status capture(opara_exec& ex, const opara_exec::Plan& p, bool traced, opa
     const int64_t v = p.order[k];
     cudaStream_t s = streams[p.stream_of[v]];
     for (int64_t u : waits[v]) CAP(cudaStreamWaitEvent(s, done[u], 0));
+    opara::g_launch_priority = ex.prio.empty() ? 0 : ex.prio[v];
     st = opara::launch_op(ex.ops[v], s, traced ? ex.trace_buf + 2 * v : nullptr, nullptr, false);
+    opara::g_launch_priority = 0;
     if (st != OPARA_OK) goto abort_capture;
     if (records[v]) CAP(cudaEventRecord(done[v], s));
   }
@@ -276,7 +288,7 @@ opara_status capture(opara_exec& ex, const opara_exec::Plan& p, bool traced, opa
       }
     }
     out->graph = g;
-    cudaError_t e = cudaGraphInstantiate(&out->exec, g, 0);
+    cudaError_t e = cudaGraphInstantiate(&out->exec, g, ex.prio.empty() ? 0 : cudaGraphInstantiateFlagUseNodePriority);
     if (e != cudaSuccess) {
       st = cuda_fail(e, "cudaGraphInstantiate");
       cudaGraphDestroy(g);
@@ -387,6 +399,19 @@ opara_status opara_exec_capture(opara_exec* ex, int32_t slot, const int32_t* str
   st = ensure_graph(*ex, slot, false, &g);
   if (st != OPARA_OK) ex->plans.erase(slot);
   return st;
+}
+
+opara_status opara_exec_set_priorities(opara_exec* ex, const int32_t* prio) {
+  if (!ex) return fail(OPARA_ERR_VALUE, "null executor");
+  if (!prio) {
+    ex->prio.clear();
+    return OPARA_OK;
+  }
+  int lo = 0, hi = 0;
+  OPARA_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));   // lo = least (0), hi = greatest (negative)
+  ex->prio.assign(prio, prio + ex->ops.size());
+  for (auto& p : ex->prio) p = std::max(hi, std::min(lo, p));
+  return OPARA_OK;
 }
 
 opara_status opara_exec_replay(opara_exec* ex, int32_t slot, void* stream) {

@@ -293,7 +293,7 @@ class ScheduledGraph:
     def __init__(self, program: Program, device: int, policy: str = "opara",
                  gpu_config: GpuConfig | None = None, profile_reps: int = 20, seed: int | None = None,
                  conv_engine: str = "tc", bound_grids: bool = False, tune: bool = True,
-                 splitk: str = "push", bound_scale: float = 1.0):
+                 splitk: str = "push", bound_scale: float = 1.0, priorities: bool | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ScheduledGraph needs a CUDA device (there is no CPU fallback)")
         self.program = program
@@ -349,6 +349,8 @@ class ScheduledGraph:
         self.schedule = make_order(self.graph, policy, self.gpu_config, seed)
         self.seq_plan = single_stream_plan(self.graph)
         self.seq_schedule = LaunchSchedule(tuple(self.graph.topo_sort()), "sequential")
+        if priorities if priorities is not None else os.environ.get("OPARA_PRIORITY") == "1":
+            self.set_priorities(self.critical_priorities())
         self.capture(SLOT_PARALLEL, self.plan, self.schedule)
         self.capture(SLOT_SEQUENTIAL, self.seq_plan, self.seq_schedule)
 
@@ -580,6 +582,36 @@ class ScheduledGraph:
         _lib.check(_lib.lib().opara_exec_capture(self._h, slot, _lib.ptr(stream_of),
                                                  int(plan.num_streams), _lib.ptr(order),
                                                  _lib.ptr(sync), len(plan.sync_events)))
+
+    def critical_priorities(self, slack_us: float = 1.0) -> np.ndarray:
+        """CUDA priority per op: the most urgent level for ops on (or within
+        `slack_us` of) the critical path of isolated kernel times, default for
+        the rest, so concurrent off-path branches yield SMs to the path that
+        sets the latency."""
+        n = len(self.program.ops)
+        t = [p["isolated_us"] for p in self.profile]
+        preds = [[] for _ in range(n)]
+        succs = [[] for _ in range(n)]
+        for u, v in self.program.edges:
+            preds[v].append(u)
+            succs[u].append(v)
+        down = [0.0] * n            # longest path from the start through op k (inclusive)
+        for v in range(n):          # ops are in topological order
+            down[v] = t[v] + max((down[u] for u in preds[v]), default=0.0)
+        up = [0.0] * n              # longest path from op k (inclusive) to the end
+        for v in reversed(range(n)):
+            up[v] = t[v] + max((up[w] for w in succs[v]), default=0.0)
+        cp = max(down) if n else 0.0
+        prio = np.zeros(n, dtype=np.int32)
+        for k in range(n):
+            if cp - (down[k] + up[k] - t[k]) <= slack_us:
+                prio[k] = -100      # clamped to the device's greatest priority
+        return prio
+
+    def set_priorities(self, prio) -> None:
+        """Per-op CUDA scheduling priorities for graphs captured afterwards (None clears)."""
+        arr = None if prio is None else np.ascontiguousarray(prio, dtype=np.int32)
+        _lib.check(_lib.lib().opara_exec_set_priorities(self._h, None if arr is None else _lib.ptr(arr)))
 
     def replay(self, slot: int = SLOT_PARALLEL, stream: torch.cuda.Stream | None = None) -> None:
         s = stream or torch.cuda.current_stream(self.dev)
