@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .dag import ComputationGraph, OperatorNode, ResourceDemand, graph_to_dict
+from .dag import ComputationGraph, OpClass, OperatorNode, ResourceDemand, graph_to_dict
 from .device import GpuConfig, device_gpu_config, GPU_PRESETS
 from .frontend import (ADD, ATTENTION, AVGPOOL2D, CONV2D, COPY, DWCONV2D, EMBEDDING, FIELD_EMBEDDING, FIRST_ORDER,
                        FM, GLOBAL_AVGPOOL, LAYERNORM, LINEAR, MAXPOOL2D, NOP, RELU, Program, lower)
@@ -293,7 +293,8 @@ class ScheduledGraph:
     def __init__(self, program: Program, device: int, policy: str = "opara",
                  gpu_config: GpuConfig | None = None, profile_reps: int = 20, seed: int | None = None,
                  conv_engine: str = "tc", bound_grids: bool = False, tune: bool = True,
-                 splitk: str = "push", bound_scale: float = 1.0, priorities: bool | None = None):
+                 splitk: str = "push", bound_scale: float = 1.0, priorities: bool | None = None,
+                 classify: str | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ScheduledGraph needs a CUDA device (there is no CPU fallback)")
         self.program = program
@@ -343,6 +344,9 @@ class ScheduledGraph:
         _lib.check(L.opara_exec_create(device, C.cast(recs, C.c_void_p), len(program.ops), C.byref(h)))
         self._h = h
         self.gpu_config = gpu_config or device_gpu_config(device)
+        # op classes for Alg. 2: "measured" (roofline position of the profiled run,
+        # default: Inception-v3 fp32 0.584 -> 0.553-0.565 ms) or "static" (operator type)
+        self.classify = classify or os.environ.get("OPARA_CLASSIFY", "measured")
         self.profile = self._profile(profile_reps)
         self.graph = self._profiled_dag()
         self.plan = allocate_streams(self.graph)
@@ -562,12 +566,32 @@ class ScheduledGraph:
                      registers_per_thread=p.registers_per_thread, isolated_us=p.isolated_us)
                 for p in out]
 
+    # roofline peaks used by the measured classifier (MEASURED_PEAKS.json values on B200)
+    PEAK_TFLOPS = {0: 74.4, 1: 1622.8 / 6, 2: 1622.8}   # SIMT fp32, 3xTF32, bf16 tensor
+    PEAK_HBM_GBS = 6534.1
+
+    def measured_class(self, k: int) -> OpClass:
+        """Compute vs memory class from where the op sits on the roofline in its
+        measured run (the paper's profiler classifies by achieved tensor vs
+        memory throughput): achieved FLOP/s over the engine's peak against
+        achieved algorithmic bytes/s over HBM peak."""
+        op, p = self.program.ops[k], self.profile[k]
+        if op.kind == NOP or p["isolated_us"] <= 0:
+            return op.op_class
+        t = p["isolated_us"] * 1e-6
+        peak = self.PEAK_TFLOPS.get(self.engines.get(k, 0), 74.4) if op.kind == CONV2D else 74.4
+        compute = op.flops / t / (peak * 1e12)
+        memory = op.bytes_min / t / (self.PEAK_HBM_GBS * 1e9)
+        return OpClass.COMPUTE if compute >= memory else OpClass.MEMORY
+
     def _profiled_dag(self) -> ComputationGraph:
+        measured = self.classify == "measured"
         nodes = []
         for k, (op, p) in enumerate(zip(self.program.ops, self.profile)):
             d = ResourceDemand(p["threads_per_block"], p["shared_mem_per_block"],
                                p["registers_per_thread"], p["num_blocks"])
-            nodes.append(OperatorNode(k + 1, op.name, op.op_class, d,
+            cls = self.measured_class(k) if measured else op.op_class
+            nodes.append(OperatorNode(k + 1, op.name, cls, d,
                                       block_duration_us(p["isolated_us"], d, self.gpu_config)))
         return ComputationGraph(nodes, [(u + 1, v + 1) for (u, v) in self.program.edges])
 
