@@ -62,6 +62,9 @@ struct BfArgs {
   int M, K, kblocks;
   int splits, kb_per_split;
   int push, rows_per;   // split-K reduction: 1 = partials pushed to the owner CTA (st.async)
+  int glob;             // split-K reduction through an L2 workspace + last-arrival CTA (no cluster)
+  float* ws;
+  unsigned* cnt;
   // fused residual + LayerNorm over all Cout channels (cluster spans the m-tiles)
   int ln, res_cs;
   const __nv_bfloat16* res;
@@ -403,6 +406,61 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     trace_end(trace);
     return;
   }
+  if (a.glob) {
+    // Split-K through L2 without a cluster: every split stores its partial
+    // [BN][128] tile to the workspace (coalesced along channels), the last CTA
+    // to arrive on the tile's counter sums the splits in z order (deterministic)
+    // and runs the epilogue; no cluster launch, no DSMEM, no co-scheduling.
+    const int tiles = gridDim.x * gridDim.y, tile = blockIdx.x + blockIdx.y * gridDim.x;
+    const int64_t plane = static_cast<int64_t>(BN) * 128;
+    if (warp < 4) {
+      tc::mbar_wait(accum, 0);
+      tc::tc_fence_after();
+      const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+      float* mine = a.ws + (static_cast<int64_t>(blockIdx.z) * tiles + tile) * plane + warp * 32 + lane;
+#pragma unroll 4
+      for (int c8 = 0; c8 < BN / 8; ++c8) {
+        float v[8];
+        tc::tmem_ld8(trow + c8 * 8, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) __stcg(mine + (c8 * 8 + e) * 128, v[e]);
+      }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tc::tc_fence_after();
+      tc::tmem_dealloc(tmem, kTmemCols);
+    }
+    if (!splitk_arrive_last(a.cnt + tile, a.splits)) {
+      trace_end(trace);
+      return;
+    }
+    TO* out = static_cast<TO*>(a.out);
+    for (int idx = tid; idx < BN * 32; idx += kThreads) {
+      const int col = idx >> 5, r4 = (idx & 31) * 4;
+      const int p = n0 + col, ch0 = mt * 128 + r4;
+      if (p >= a.M) continue;
+      const float* src = a.ws + static_cast<int64_t>(tile) * plane + col * 128 + r4;
+      float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+      for (int z = 1; z < a.splits; ++z) {
+        const float4 q = __ldcg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(z) * tiles * plane));
+        acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+      }
+      const float y[4] = {acc.x, acc.y, acc.z, acc.w};
+      TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (ch0 + e < a.Cout) {
+          const float o = act_fn(y[e] + (a.bias ? __ldg(a.bias + ch0 + e) : 0.f), a.act);
+          if constexpr (std::is_same<TO, float>::value) dst[e] = o;
+          else dst[e] = __float2bfloat16_rn(o);
+        }
+      }
+    }
+    trace_end(trace);
+    return;
+  }
   if (push) {
     // TMEM -> registers -> st.async of 4-column float4 groups straight into the
     // owning rank's receive buffer (slot = my rank); the owner's mbarrier
@@ -708,6 +766,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
     a.splits = 1;
     a.kb_per_split = a.kblocks;
     a.push = 0;
+    a.glob = 0;
     a.rows_per = v[lid].bn;
     LaunchCfg c;
     c.func = v[lid].func[mode][out_f32 ? 1 : 0];
@@ -742,7 +801,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   splits = std::min<int64_t>(splits, std::max(1, a.kblocks / 2));
   splits = std::max<int64_t>(1, splits);
   const void* func = v[id].func[mode][out_f32 ? 1 : 0];
-  if (splits > 1 && op.i[19] <= 1)
+  if (splits > 1 && op.i[19] <= 1 && op.i[26] != 2)   // (the L2 reduction needs no co-resident cluster)
     while (splits > 1) {
       const int rp = ((bn + static_cast<int>(splits) - 1) / static_cast<int>(splits) + 3) / 4 * 4;
       const size_t rb = static_cast<size_t>(splits) * 128 * rp * 4;
@@ -760,17 +819,29 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
   a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
             !push_disabled() && op.i[26] == 0) ? 1 : 0;
+  a.glob = (a.splits > 1 && op.i[26] == 2) ? 1 : 0;   // reduction through an L2 workspace
   LaunchCfg c;
   c.func = func;
   c.grid = dim3(ceil_div(a.M, bn), mtiles, a.splits);
   c.block = dim3(kThreads);
   c.smem = v[id].smem + (a.push ? recv_bytes : 0);
+  const int64_t tiles = static_cast<int64_t>(c.grid.x) * c.grid.y;
+  const int64_t ws_floats = a.glob ? static_cast<int64_t>(a.splits) * tiles * bn * 128 : 0;
+  c.workspace = a.glob ? splitk_workspace_bytes(ws_floats, tiles) : 0;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
+  if (a.glob) {
+    if (!op.p[7]) return fail(OPARA_ERR_INTERNAL, "conv2d_tc_bf16: split-K workspace missing");
+    a.ws = static_cast<float*>(op.p[7]);
+    a.cnt = splitk_counters(op.p[7], ws_floats);
+  } else {
+    a.ws = nullptr;
+    a.cnt = nullptr;
+  }
   opara_status st = set_attr_once(func, attr_smem(v[id].smem));
   if (st != OPARA_OK) return st;
   void* args[] = {&a, &trace};
-  return launch_kernel(c, args, s, a.splits > 1 ? static_cast<unsigned>(a.splits) : 1u);
+  return launch_kernel(c, args, s, (a.splits > 1 && !a.glob) ? static_cast<unsigned>(a.splits) : 1u);
 }
 
 }  // namespace opara

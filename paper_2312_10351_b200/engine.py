@@ -180,8 +180,11 @@ def concurrency_targets(program: Program, num_sms: int = 148, scale: float = 1.0
     return out
 
 
+SPLITK_MODES = {"push": 0, "pull": 1, "global": 2}
+
+
 def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0,
-               splitk_pull: bool = False) -> _lib.OparaOp:
+               splitk_mode: int = 0) -> _lib.OparaOp:
     """Fill the POD launch record of one lowered op (layouts: csrc/ops.h)."""
     rec = _lib.OparaOp()
     rec.kind = op.kind
@@ -198,7 +201,7 @@ def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0,
         vals = [q["N"], q["H"], q["W"], q["Cin"], ics, icoff, q["OH"], q["OW"], q["Cout"], ocs, ocoff,
                 q["R"], q["S"], q["sh"], q["sw"], q["ph"], q["pw"], q["relu"], in_dt if conv_engine == 2 else 0,
                 1, int(inchw), int(target_ctas), conv_engine, DTYPE_CODE[op.output.dtype],
-                q.get("act", 1 if q["relu"] else 0), q.get("relu_in", 0), int(splitk_pull)]
+                q.get("act", 1 if q["relu"] else 0), q.get("relu_in", 0), int(splitk_mode)]
         rec.p[0], rec.p[1], rec.p[2], rec.p[3] = ib, weights[0], weights[1], ob
     elif op.kind == DWCONV2D:
         vals = [q["N"], q["H"], q["W"], q["C"], ics, icoff, q["OH"], q["OW"], ocs, ocoff, q["kh"], q["kw"],
@@ -308,12 +311,13 @@ class ScheduledGraph:
         self.bound_grids = bool(bound_grids)
         self.bound_scale = bound_scale
         # split-K reduction: "push" (st.async partials to the owner CTA), "pull" (DSMEM after a
-        # cluster barrier), or "auto": pull where other convs share the DAG level (concurrent
-        # branches), push for convs that run alone
+        # cluster barrier), "global" (bf16 engine: partials through an L2 workspace, last CTA
+        # reduces, no cluster), or "auto": pull where other convs share the DAG level
+        # (concurrent branches), push for convs that run alone
         self.splitk = splitk
         conc = concurrent_convs(program) if splitk == "auto" else {}
-        pull_of = {k: (splitk == "pull") or (splitk == "auto" and conc.get(k, 1) > 1)
-                   for k in range(len(program.ops))}
+        mode_of = {k: (SPLITK_MODES["pull"] if conc.get(k, 1) > 1 else SPLITK_MODES["push"]) if splitk == "auto"
+                   else SPLITK_MODES[splitk] for k in range(len(program.ops))}
         self.targets = concurrency_targets(program, scale=bound_scale) if bound_grids else {}
         for k, op in enumerate(program.ops):
             if op.kind in ROW_KINDS:
@@ -321,7 +325,7 @@ class ScheduledGraph:
             else:
                 recs[k] = _op_record(op, self._views(op), self._weights(op),
                                      conv_engine_for(op, self.conv_engine), self.targets.get(k, 0),
-                                     pull_of[k])
+                                     mode_of[k])
                 if op.kind == CONV2D and op.ints.get("ln"):   # fused residual + LayerNorm epilogue
                     (rb, rcoff, rcs, _), = self._all_views(op)[1:2]
                     arr = self._arrays(op)
