@@ -48,7 +48,19 @@ __host__ __device__ constexpr int bf_stages(int bn) { return bn == 16 ? 24 : bn 
 // full[], empty[], accum, tmem slot, push barrier: rounded up to 128 bytes
 __host__ __device__ constexpr int bf_bar_bytes(int stages) { return ((2 * stages + 3) * 8 + 127) / 128 * 128; }
 
-enum GatherMode { kVecBf16 = 0, kScalarBf16 = 1, kScalarF32 = 2 };
+// kVecBf16: 16-byte cp.async of 8 channels (Cin % 8 == 0); kSub4 / kSub2: each
+// 16-byte smem chunk assembled from 8- / 4-byte cp.asyncs of 4 / 2 channels
+// (Cin % 4 / % 2 == 0, e.g. NASNet's 84 / 42 channels), every sub-chunk with
+// its own incrementally tracked (r, s, c); scalar register paths otherwise.
+enum GatherMode { kVecBf16 = 0, kScalarBf16 = 1, kScalarF32 = 2, kSub4 = 3, kSub2 = 4 };
+constexpr int kModes = 5;
+
+__device__ __forceinline__ void cp_async_sub(uint32_t dst, const void* src, int bytes, bool ok) {
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
 
 struct BfArgs {
   const void* in;
@@ -182,6 +194,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     }
     pdl_wait();
     trace_begin(trace);
+    // Fused input ReLU (relu_in): the copies of stage i are committed as one
+    // cp.async group; once stage i-1's group has landed this thread clamps
+    // its own chunks of it in place (bf16 max with 0), fences them into the
+    // async proxy and arrives, so the transform trails the gather by a stage.
+    auto relu_stage = [&](int st) {
+      uint8_t* xs_g = smem + st * kStage + kWBytes;
+#pragma unroll
+      for (int j = 0; j < kRowsPerThread; ++j) {
+        if (rw + 4 * j >= kRowGroups) break;
+        uint4* q = reinterpret_cast<uint4*>(xs_g + x_off(j));
+        uint4 v = *q;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+        const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = __hmax2(h[e], z);
+        *q = v;
+      }
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&full[st]);
+    };
     if constexpr (kMode == kVecBf16) {
       const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(a.in);
       const __nv_bfloat16* rowbase[kRowsPerThread];
@@ -195,26 +227,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
         dr = rs / a.S;
         dq = rs - dr * a.S;
       }
-      // Fused input ReLU (relu_in): the copies of stage i are committed as one
-      // cp.async group; once stage i-1's group has landed this thread clamps
-      // its own chunks of it in place (bf16 max with 0), fences them into the
-      // async proxy and arrives, so the transform trails the gather by a stage.
-      auto relu_stage = [&](int st) {
-        uint8_t* xs_g = smem + st * kStage + kWBytes;
-#pragma unroll
-        for (int j = 0; j < kRowsPerThread; ++j) {
-          if (rw + 4 * j >= kRowGroups) break;
-          uint4* q = reinterpret_cast<uint4*>(xs_g + x_off(j));
-          uint4 v = *q;
-          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
-          const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) h[e] = __hmax2(h[e], z);
-          *q = v;
-        }
-        tc::fence_proxy_async_smem();
-        tc::mbar_arrive(&full[st]);
-      };
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
@@ -244,6 +256,64 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
             dq = 0;
             ++dr;
           }
+        }
+      }
+      if (a.relu_in && nkb > 0) {
+        cp_async_wait<0>();
+        relu_stage((nkb - 1) % kStages);
+      }
+    } else if constexpr (kMode == kSub4 || kMode == kSub2) {
+      constexpr int G = kMode == kSub4 ? 4 : 2;   // channels per cp.async
+      constexpr int NS = 8 / G;                   // sub-chunks per 16-byte chunk
+      const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(a.in);
+      const __nv_bfloat16* rowbase[kRowsPerThread];
+#pragma unroll
+      for (int j = 0; j < kRowsPerThread; ++j)
+        rowbase[j] = in + (pb[j] >= 0 ? pb[j] * a.sN + pih[j] * a.sH + piw[j] * a.sW + a.in_coff : 0);
+      int kc[NS], dc[NS], dr[NS], dq[NS];
+#pragma unroll
+      for (int u = 0; u < NS; ++u) {
+        kc[u] = kb0 * kBK + cl * 8 + u * G;
+        dc[u] = dr[u] = dq[u] = 0;
+        if (kc[u] < a.K) {
+          dc[u] = kc[u] % a.Cin;
+          const int rs = kc[u] / a.Cin;
+          dr[u] = rs / a.S;
+          dq[u] = rs - dr[u] * a.S;
+        }
+      }
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        const uint32_t xs = tc::smem_u32(smem + s * kStage + kWBytes);
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+          const bool kin = kc[u] < a.K;
+          const int64_t koff = dr[u] * a.sH + dq[u] * a.sW + dc[u];
+#pragma unroll
+          for (int j = 0; j < kRowsPerThread; ++j) {
+            const int ih = pih[j] + dr[u], iw = piw[j] + dq[u];
+            const bool ok = kin && pb[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+            if (rw + 4 * j < kRowGroups) cp_async_sub(xs + x_off(j) + u * G * 2, ok ? rowbase[j] + koff : in, G * 2, ok);
+          }
+          kc[u] += kBK;
+          dc[u] += kBK;
+          while (dc[u] >= a.Cin) {
+            dc[u] -= a.Cin;
+            if (++dq[u] == a.S) {
+              dq[u] = 0;
+              ++dr[u];
+            }
+          }
+        }
+        if (a.relu_in) {
+          cp_async_commit();
+          if (i > 0) {
+            cp_async_wait<1>();
+            relu_stage((i - 1) % kStages);
+          }
+        } else {
+          tc::cp_async_arrive_noinc(&full[s]);
         }
       }
       if (a.relu_in && nkb > 0) {
@@ -624,7 +694,7 @@ constexpr size_t bf_smem_bytes() {
 
 struct BfVariant {
   int bn;
-  const void* func[3][2];  // [gather mode][out bf16, out f32]
+  const void* func[kModes][2];  // [gather mode][out bf16, out f32]
   size_t smem;
 };
 
@@ -638,6 +708,10 @@ BfVariant make_bf() {
   v.func[kScalarBf16][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kScalarBf16, float>);
   v.func[kScalarF32][0] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kScalarF32, __nv_bfloat16>);
   v.func[kScalarF32][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kScalarF32, float>);
+  v.func[kSub4][0] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kSub4, __nv_bfloat16>);
+  v.func[kSub4][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kSub4, float>);
+  v.func[kSub2][0] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kSub2, __nv_bfloat16>);
+  v.func[kSub2][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kSub2, float>);
   v.smem = bf_smem_bytes<BN>();
   return v;
 }
@@ -741,9 +815,11 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
     a.sN = a.sH * a.H;
   }
   if (a.M <= 0 || a.Cout <= 0 || a.K <= 0) return fail(OPARA_ERR_VALUE, "conv2d: empty shape");
-  const int mode = in_f32 ? kScalarF32
-                 : (!nchw && a.Cin % 8 == 0 && in_cs % 8 == 0 && a.in_coff % 8 == 0 &&
-                    reinterpret_cast<uintptr_t>(a.in) % 16 == 0) ? kVecBf16 : kScalarBf16;
+  auto vec_ok = [&](int g) {
+    return !nchw && a.Cin % g == 0 && in_cs % g == 0 && a.in_coff % g == 0 &&
+           reinterpret_cast<uintptr_t>(a.in) % (2 * g) == 0;
+  };
+  const int mode = in_f32 ? kScalarF32 : vec_ok(8) ? kVecBf16 : vec_ok(4) ? kSub4 : vec_ok(2) ? kSub2 : kScalarBf16;
   const int align = out_f32 ? 16 : 8;
   a.vec_out = (a.out_cs % 4 == 0 && a.out_coff % 4 == 0 && reinterpret_cast<uintptr_t>(a.out) % align == 0) ? 1 : 0;
   const BfVariant* v = bf_variants();
