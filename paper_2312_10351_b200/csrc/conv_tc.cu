@@ -759,7 +759,7 @@ const TcVariant* tc_variants(int* count) {
 }
 
 constexpr size_t kPushMaxBytes = 48 * 1024;
-constexpr size_t kSmemLimit = 232448;   // 227 KB of opt-in dynamic smem per CTA (sm_100)
+constexpr size_t kSmemLimit = 232448 - 1024;   // 227 KB opt-in smem per CTA, minus static smem headroom
 inline size_t attr_smem(size_t ring) { return std::min(ring + kPushMaxBytes, kSmemLimit); }
 
 bool push_disabled() {
