@@ -11,6 +11,8 @@
 // arrival counter) reduces the partials in split order — deterministic — and
 // runs the epilogue.  The tensor-core engines live in conv_tc.cu.
 
+#include <cuda_bf16.h>
+
 #include "device_common.cuh"
 #include "ops.h"
 #include "status.h"
@@ -22,13 +24,13 @@ struct ConvArgs {
   const float* __restrict__ in;
   const float* __restrict__ w;
   const float* __restrict__ bias;
-  float* __restrict__ out;
+  float* __restrict__ out;      // fp32 output, or bf16 when out_bf16 (bf16 models' fp32-input stems)
   float* __restrict__ ws;       // [splits][M][Cout] partials (split-K only)
   unsigned* __restrict__ cnt;   // per output tile arrival counters (split-K only)
   int N, H, W, Cin, in_cs, in_coff;
   int OH, OW, Cout, out_cs, out_coff;
   int R, S, sh, sw, ph, pw;
-  int relu, relu_in;
+  int relu, relu_in, out_bf16;
   int M, K;
   int splits, kt_per_split;
   // input element (b, ih, iw, c) lives at in[b*sN + ih*sH + iw*sW + c*sC + in_coff]
@@ -196,13 +198,15 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     const int m = m0 + ty * TM + i;
     if (m >= a.M) continue;
     float* orow = a.out + static_cast<int64_t>(m) * a.out_cs + a.out_coff;
+    __nv_bfloat16* orow_bf = reinterpret_cast<__nv_bfloat16*>(a.out) + static_cast<int64_t>(m) * a.out_cs + a.out_coff;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       const int n = n0 + tx * TN + j;
       if (n < a.Cout) {
         float v = acc[i][j] + (a.bias ? __ldg(a.bias + n) : 0.f);
         if (a.relu) v = apply_act(v, a.relu);
-        orow[n] = v;
+        if (a.out_bf16) orow_bf[n] = __float2bfloat16_rn(v);
+        else orow[n] = v;
       }
     }
   }
@@ -288,7 +292,8 @@ opara_status launch_conv2d(const opara_op& op, cudaStream_t s, unsigned long lon
   a.ph = (int)op.i[15]; a.pw = (int)op.i[16];
   a.relu = conv_act_code(op.i[24], op.i[17]);   // `relu` carries the activation code
   a.relu_in = (int)op.i[25];
-  if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "conv2d simt engine: fp32 only");
+  a.out_bf16 = op.i[23] == 1 ? 1 : 0;   // record i[23]: output dtype (0 fp32, 1 bf16)
+  if (op.i[18] != 0) return fail(OPARA_ERR_VALUE, "conv2d simt engine: fp32 input only");
   a.M = a.N * a.OH * a.OW;
   a.K = a.R * a.S * a.Cin;
   const bool nchw = op.i[20] != 0;

@@ -77,6 +77,7 @@ struct BfArgs {
   int glob;             // split-K reduction through an L2 workspace + last-arrival CTA (no cluster)
   float* ws;
   unsigned* cnt;
+  const int4* ktab;     // scalar gathers: per k (dr, dq, input offset) from the host (no divisions)
   // fused residual + LayerNorm over all Cout channels (cluster spans the m-tiles)
   int ln, res_cs;
   const __nv_bfloat16* res;
@@ -333,12 +334,21 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
         for (int e = 0; e < 8; ++e) {
           const int k = kbase + e;
           const bool kin = k < a.K;
-          int c = 0, r = 0, q = 0;
+          int r = 0, q = 0;
+          int64_t koff = 0;
           if (kin) {
-            c = k % a.Cin;
-            const int rs = k / a.Cin;
-            r = rs / a.S;
-            q = rs - r * a.S;
+            if (a.ktab) {   // host-built (dr, dq, offset) per k: no integer divisions per element
+              const int4 t = __ldg(a.ktab + k);
+              r = t.x;
+              q = t.y;
+              koff = t.z;
+            } else {
+              const int c = k % a.Cin;
+              const int rs = k / a.Cin;
+              r = rs / a.S;
+              q = rs - r * a.S;
+              koff = r * a.sH + q * a.sW + c * a.sC;
+            }
           }
 #pragma unroll
           for (int j = 0; j < kRowsPerThread; ++j) {
@@ -346,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
             const bool ok = kin && pb[j] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
             float x = 0.f;
             if (ok) {
-              const TIn t = in[pb[j] * a.sN + ih * a.sH + iw * a.sW + c * a.sC + a.in_coff];
+              const TIn t = in[pb[j] * a.sN + pih[j] * a.sH + piw[j] * a.sW + koff + a.in_coff];
               if constexpr (kMode == kScalarF32) x = t; else x = __bfloat162float(t);
               if (a.relu_in) x = fmaxf(x, 0.f);
             }
@@ -824,6 +834,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   a.vec_out = (a.out_cs % 4 == 0 && a.out_coff % 4 == 0 && reinterpret_cast<uintptr_t>(a.out) % align == 0) ? 1 : 0;
   const BfVariant* v = bf_variants();
   const int mtiles = (a.Cout + 127) / 128;
+  a.ktab = (op.i[27] == 0) ? static_cast<const int4*>(op.p[5]) : nullptr;
   a.ln = static_cast<int>(op.i[27]);
   a.res = static_cast<const __nv_bfloat16*>(op.p[4]);
   a.res_cs = static_cast<int>(op.i[28]);

@@ -326,6 +326,10 @@ class ScheduledGraph:
                 recs[k] = _op_record(op, self._views(op), self._weights(op),
                                      conv_engine_for(op, self.conv_engine), self.targets.get(k, 0),
                                      mode_of[k])
+                if op.kind == CONV2D and recs[k].i[22] == 2 and not op.ints.get("ln"):
+                    ktab = self._gather_table(op)
+                    if ktab is not None:
+                        recs[k].p[5] = ktab
                 if op.kind == CONV2D and op.ints.get("ln"):   # fused residual + LayerNorm epilogue
                     (rb, rcoff, rcs, _), = self._all_views(op)[1:2]
                     arr = self._arrays(op)
@@ -411,6 +415,27 @@ class ScheduledGraph:
             ptrs[name] = t.data_ptr()
         return ptrs
 
+    def _gather_table(self, op):
+        """Device table of (dr, dq, input offset) per k for the bf16 engine's
+        scalar gathers (fp32 NCHW graph input, odd channel counts), so the
+        kernel does no integer division per gathered element."""
+        x = op.inputs[0].root()[0]
+        q = op.ints
+        if not (x.nchw_input or x.dtype == "f32" or q["Cin"] % 2):
+            return None
+        n, h, w, cin = x.shape
+        if x.nchw_input:
+            s_c, s_w, s_h = h * w, 1, w
+        else:
+            s_c, s_w, s_h = 1, x.shape[-1], w * x.shape[-1]
+        k = np.arange(q["R"] * q["S"] * q["Cin"])
+        c, rs = k % q["Cin"], k // q["Cin"]
+        r, s_ = rs // q["S"], rs % q["S"]
+        tab = np.stack([r, s_, r * s_h + s_ * s_w + c * s_c, np.zeros_like(k)], axis=1).astype(np.int32)
+        t = torch.from_numpy(np.ascontiguousarray(tab)).to(self.dev)
+        self._keep.append(t)
+        return t.data_ptr()
+
     def _weights(self, op):
         ptrs = []
         weight = op.weight
@@ -465,9 +490,10 @@ class ScheduledGraph:
                 continue
             k0 = ks[0]
             budget = self.targets.get(k0, 0)
-            if recs[k0].i[22] == 1:
-                # fp32 convs may also run on the exact-FFMA SIMT engine (no TMEM / cluster
-                # overheads): let measurement decide per shape
+            if recs[k0].i[22] == 1 or (recs[k0].i[22] == 2 and recs[k0].i[18] == 0):
+                # convs over fp32 inputs (fp32 models, and bf16 models' stems over the fp32
+                # NCHW image) may also run on the exact-FFMA SIMT engine (no TMEM / cluster
+                # overheads; it stores bf16 for bf16 models): let measurement decide per shape
                 t = torch.from_numpy(np.ascontiguousarray(self.program.ops[k0].weight)).to(self.dev)
                 self._keep.append(t)
                 simt_w[k0] = t.data_ptr()

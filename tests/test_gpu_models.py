@@ -141,3 +141,21 @@ def test_splitk_reductions_agree(splitk):
     with torch.no_grad():
         ref = model.cuda()(x.cuda())
     assert _rel(y, ref) <= 1e-2
+
+
+def test_cli_measure_runs_every_policy(tmp_path):
+    """`python -m paper_2312_10351_b200 measure`: the same kernels and Alg. 1 plan
+    captured under each launch policy, all timed on the device."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    out = tmp_path / "m.json"
+    r = subprocess.run([sys.executable, "-m", "paper_2312_10351_b200", "measure", "googlenet", "--grids", "full",
+                        "--iters", "10", "--out", str(out)], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rows = {row["policy"]: row for row in json.loads(out.read_text())["rows"]}
+    assert set(rows) == {"sequential", "opara", "dfs", "wavefront", "random"}
+    assert rows["sequential"]["num_streams"] == 1 and rows["opara"]["num_streams"] == 28
+    assert all(row["latency_ms"] > 0 for row in rows.values())
