@@ -293,7 +293,7 @@ def run_gpu(args) -> dict | None:
         else:
             name = {2: "maxpool2d", 3: "avgpool2d", 4: "global_avgpool", 5: "linear_f32", 6: "add",
                     7: "layernorm", 9: "embedding", 10: "attention_tc", 11: "copy", 12: "fm", 13: "dwconv2d",
-                    14: "relu", 16: "field_embedding", 17: "first_order"}[op.kind]
+                    14: "relu", 16: "field_embedding", 17: "first_order", 18: "pack_input"}[op.kind]
         f = fam.setdefault(name, {"us": 0.0, "flops": 0, "bytes": 0, "launches": 0})
         f["us"] += p["isolated_us"]
         f["flops"] += op.flops

@@ -186,7 +186,8 @@ typedef enum opara_op_kind {
   OPARA_OP_RELU = 14,       /* unfused ReLU over a channel view                           */
   OPARA_OP_SOFTMAX = 15,    /* reserved                                                   */
   OPARA_OP_FIELD_EMBEDDING = 16, /* per-field embedding row gather into a slice (deepfm.cu) */
-  OPARA_OP_FIRST_ORDER = 17 /* DeepFM linear part: sum of per-field weights + dense dot    */
+  OPARA_OP_FIRST_ORDER = 17, /* DeepFM linear part: sum of per-field weights + dense dot   */
+  OPARA_OP_PACK_INPUT = 18  /* fp32 NCHW image -> NHWC bf16 with channels zero-padded to 8 */
 } opara_op_kind;
 
 #define OPARA_OP_MAX_INTS 40

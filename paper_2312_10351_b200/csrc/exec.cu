@@ -100,6 +100,7 @@ opara_status launch_op(const opara_op& op, cudaStream_t s, unsigned long long* t
     case OPARA_OP_FIELD_EMBEDDING:
     case OPARA_OP_FIRST_ORDER:
     case OPARA_OP_FM: return launch_deepfm(op, s, trace, cfg, dry);
+    case OPARA_OP_PACK_INPUT: return launch_pack_input(op, s, trace, cfg, dry);
     default: return fail(OPARA_ERR_VALUE, "unsupported op kind " + std::to_string(op.kind));
   }
 }

@@ -32,12 +32,12 @@ from . import _lib
 from .dag import ComputationGraph, OpClass, OperatorNode, ResourceDemand, graph_to_dict
 from .device import GpuConfig, device_gpu_config, GPU_PRESETS
 from .frontend import (ADD, ATTENTION, AVGPOOL2D, CONV2D, COPY, DWCONV2D, EMBEDDING, FIELD_EMBEDDING, FIRST_ORDER,
-                       FM, GLOBAL_AVGPOOL, LAYERNORM, LINEAR, MAXPOOL2D, NOP, RELU, Program, lower)
+                       FM, GLOBAL_AVGPOOL, LAYERNORM, LINEAR, MAXPOOL2D, NOP, PACK_INPUT, RELU, Program, lower)
 from .order import LaunchSchedule, make_order
 from .plan import StreamPlan, allocate_streams, plan_to_dict, single_stream_plan
 
 # kinds whose records are built from every input view + named host arrays
-ROW_KINDS = (LAYERNORM, EMBEDDING, ATTENTION, ADD, COPY, RELU, FIELD_EMBEDDING, FIRST_ORDER, FM)
+ROW_KINDS = (LAYERNORM, EMBEDDING, ATTENTION, ADD, COPY, RELU, FIELD_EMBEDDING, FIRST_ORDER, FM, PACK_INPUT)
 
 SLOT_PARALLEL = 0
 SLOT_SEQUENTIAL = 1
@@ -248,6 +248,10 @@ def _row_record(rec, op, views, arrays):
             rec.p[slots[j]] = ib
         vals += [0] * 4 + [DTYPE_CODE[op.output.dtype]]
         rec.p[3] = ob
+    elif op.kind == PACK_INPUT:
+        (ib, _, _, _), = ins
+        vals = [q["N"], q["H"], q["W"], q["C"], q["Cp"]]
+        rec.p[0], rec.p[3] = ib, ob
     elif op.kind == FIELD_EMBEDDING:
         (ib, icoff, ics, _), = ins
         vals = [q["B"], q["dim"], q["field"] + icoff, ics, ocs, ocoff, q["vocab"]]

@@ -30,7 +30,7 @@ from .dag import OpClass
 # opara_op_kind values (include/opara.h)
 NOP, CONV2D, MAXPOOL2D, AVGPOOL2D, GLOBAL_AVGPOOL, LINEAR, ADD = 0, 1, 2, 3, 4, 5, 6
 LAYERNORM, EMBEDDING, ATTENTION, COPY, FM, DWCONV2D, RELU = 7, 9, 10, 11, 12, 13, 14
-FIELD_EMBEDDING, FIRST_ORDER = 16, 17
+FIELD_EMBEDDING, FIRST_ORDER, PACK_INPUT = 16, 17, 18
 
 # linear + residual + LayerNorm fusion (opt-in): deepest reduction (K) one CTA streams whole.
 # Measured on BERT-base: the fused O-proj + LN (48 unsplit CTAs streaming 196 KB of weights
@@ -147,6 +147,7 @@ class _Lowerer:
         self.env: dict = {}
         self.consumed: set[fx.Node] = set()
         self._materialized: dict[int, Tensor] = {}
+        self._packed = None
 
     def new_tensor(self, shape, producers=(), dtype=None):
         t = Tensor(len(self.tensors), tuple(int(x) for x in shape), set(producers),
@@ -247,6 +248,12 @@ class _Lowerer:
         x = lz.tensor
         tail, bn, relu = self._bn_relu_tail(node)
         n, h, w, cin = x.shape
+        cin_model = cin
+        if x.nchw_input and self.act_dtype == "bf16" and cin % 8 and not lz.relu and lz.sub is None:
+            # bf16 stem over the fp32 NCHW image: read a zero-padded NHWC bf16 copy
+            # instead (one 16-byte gather per tap), weights padded to match
+            x = self._packed_input(x)
+            cin = x.shape[3]
         r, s = conv.kernel_size
         sh, sw = _pair(conv.stride)
         ph, pw = _pair(conv.padding)
@@ -263,7 +270,10 @@ class _Lowerer:
         cout = conv.out_channels
         out = self.new_tensor((n, oh, ow, cout))
         wk, b = _fold_bn(conv, bn)
-        macs = n * oh * ow * cout * r * s * cin
+        if cin != cin_model:   # zero rows for the padded input channels: k = (r*S + s)*Cin + c
+            wk = np.pad(wk.reshape(r * s, cin_model, cout), ((0, 0), (0, cin - cin_model), (0, 0))
+                        ).reshape(r * s * cin, cout)
+        macs = n * oh * ow * cout * r * s * cin_model
         op = LoweredOp(CONV2D, "conv", OpClass.COMPUTE,
                        dict(N=n, H=h, W=w, Cin=cin, OH=oh, OW=ow, Cout=cout, R=r, S=s, sh=sh,
                             sw=sw, ph=ph, pw=pw, relu=int(relu), relu_in=int(lz.relu)),
@@ -273,6 +283,17 @@ class _Lowerer:
                        label=node.name)
         self.emit(op)
         self.env[tail] = out
+
+    def _packed_input(self, x: Tensor) -> Tensor:
+        """The NHWC bf16, 8-channel-padded copy of the NCHW graph image (one PACK_INPUT op)."""
+        if getattr(self, "_packed", None) is None:
+            n, h, w, c = x.shape
+            cp = (c + 7) // 8 * 8
+            out = self.new_tensor((n, h, w, cp), dtype="bf16")
+            self.emit(LoweredOp(PACK_INPUT, "copy", OpClass.MEMORY, dict(N=n, H=h, W=w, C=c, Cp=cp), [x], out,
+                                bytes_min=4 * n * h * w * c + 2 * n * h * w * cp, label="pack_input"))
+            self._packed = out
+        return self._packed
 
     def lower_dwconv(self, node, conv: nn.Conv2d):
         lz = self.lazy(node.args[0])
