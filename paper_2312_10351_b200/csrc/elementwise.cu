@@ -123,29 +123,32 @@ __global__ void __launch_bounds__(256) ew_scalar(EwArgs a, unsigned long long* t
   trace_end(trace);
 }
 
-// PACK_INPUT: the fp32 NCHW graph image -> NHWC bf16 with the channels
-// zero-padded to Cp (a multiple of 8), so a bf16 model's stem conv gathers one
-// 16-byte vector per (pixel, tap) instead of Cin scalar fp32 loads.  Thread =
-// (pixel, 8-channel group): reads coalesced along pixels, one 16-byte store.
-__global__ void __launch_bounds__(256) pack_input_nchw(const float* __restrict__ in, __nv_bfloat16* out, int N,
-                                                       int HW, int C, int Cp, unsigned long long* trace) {
+// PACK_INPUT: the fp32 NCHW graph image -> NHWC (bf16 or fp32) with the
+// channels zero-padded to Cp (a multiple of the 16-byte vector width), so the
+// stem conv gathers one 16-byte vector per (pixel, tap) instead of Cin scalar
+// strided loads.  Thread = (pixel, channel group): reads coalesced along
+// pixels, one 16-byte store.
+template <typename T, int V>
+__global__ void __launch_bounds__(256) pack_input_nchw(const float* __restrict__ in, T* out, int N, int HW, int C,
+                                                       int Cp, unsigned long long* trace) {
   pdl_trigger();
   pdl_wait();
   trace_begin(trace);
-  const int groups = Cp / 8;
-  const int64_t total = static_cast<int64_t>(N) * HW * groups;
+  const int groups = Cp / V;
+  const int64_t npix = static_cast<int64_t>(N) * HW;
+  const int64_t total = npix * groups;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t g = t / (static_cast<int64_t>(N) * HW);
-    const int64_t q = t - g * N * HW;          // pixel index over the batch
+    const int64_t g = t / npix;
+    const int64_t q = t - g * npix;  // pixel index over the batch
     const int64_t b = q / HW, pix = q - b * HW;
-    float f[8];
+    float f[V];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int c = static_cast<int>(g) * 8 + e;
+    for (int e = 0; e < V; ++e) {
+      const int c = static_cast<int>(g) * V + e;
       f[e] = c < C ? __ldg(in + (b * C + c) * HW + pix) : 0.f;
     }
-    *reinterpret_cast<uint4*>(out + q * Cp + g * 8) = Vec<__nv_bfloat16, 8>::pack(f);
+    *reinterpret_cast<typename Vec<T, V>::raw*>(out + q * Cp + g * V) = Vec<T, V>::pack(f);
   }
   trace_end(trace);
 }
@@ -155,13 +158,16 @@ __global__ void __launch_bounds__(256) pack_input_nchw(const float* __restrict__
 opara_status launch_pack_input(const opara_op& op, cudaStream_t s, unsigned long long* trace, LaunchCfg* cfg,
                                bool dry) {
   const float* in = static_cast<const float*>(op.p[0]);
-  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(op.p[3]);
+  void* out = op.p[3];
   int N = (int)op.i[0], HW = (int)(op.i[1] * op.i[2]), C = (int)op.i[3], Cp = (int)op.i[4];
-  if (Cp % 8 || Cp < C || N <= 0 || HW <= 0) return fail(OPARA_ERR_VALUE, "pack_input: bad shape");
+  const bool bf16 = op.i[18] == 1;
+  const int V = bf16 ? 8 : 4;
+  if (Cp % V || Cp < C || N <= 0 || HW <= 0) return fail(OPARA_ERR_VALUE, "pack_input: bad shape");
   LaunchCfg c;
-  c.func = reinterpret_cast<const void*>(&pack_input_nchw);
+  c.func = bf16 ? reinterpret_cast<const void*>(&pack_input_nchw<__nv_bfloat16, 8>)
+                : reinterpret_cast<const void*>(&pack_input_nchw<float, 4>);
   c.block = dim3(256);
-  c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(static_cast<int64_t>(N) * HW * (Cp / 8), 256), 148u * 4u)));
+  c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(static_cast<int64_t>(N) * HW * (Cp / V), 256), 148u * 4u)));
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
   void* args[] = {&in, &out, &N, &HW, &C, &Cp, &trace};

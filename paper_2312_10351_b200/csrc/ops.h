@@ -27,8 +27,8 @@
 //              p: 0 in, 3 out
 // GLOBAL_AVGPOOL i: 0 N, 1 H, 2 W, 3 C, 4 in_cstride, 5 in_coff, 8 out_cstride (0 = C),
 //                 17 relu_in, 18 dtype;  p: 0 in, 3 out fp32 (first channel of the output view)
-// PACK_INPUT   i: 0 N, 1 H, 2 W, 3 C, 4 Cp (padded channels, multiple of 8);  p: 0 in (fp32 NCHW),
-//              3 out (bf16 NHWC [N][H][W][Cp])
+// PACK_INPUT   i: 0 N, 1 H, 2 W, 3 C, 4 Cp (padded channels: multiple of 8 bf16 / 4 fp32),
+//              18 out dtype;  p: 0 in (fp32 NCHW), 3 out (NHWC [N][H][W][Cp])
 // ADD / COPY / RELU, DWCONV2D, FIELD_EMBEDDING / FIRST_ORDER / FM: see the header comment of
 //              elementwise.cu, dwconv.cu and deepfm.cu
 // LINEAR       i: 0 M (rows), 1 K, 2 N (out features), 3 act (0 none, 1 relu, 2 gelu, 3 tanh),

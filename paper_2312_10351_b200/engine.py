@@ -250,7 +250,7 @@ def _row_record(rec, op, views, arrays):
         rec.p[3] = ob
     elif op.kind == PACK_INPUT:
         (ib, _, _, _), = ins
-        vals = [q["N"], q["H"], q["W"], q["C"], q["Cp"]]
+        vals = [q["N"], q["H"], q["W"], q["C"], q["Cp"]] + [0] * 13 + [DTYPE_CODE[op.output.dtype]]
         rec.p[0], rec.p[3] = ib, ob
     elif op.kind == FIELD_EMBEDDING:
         (ib, icoff, ics, _), = ins

@@ -249,9 +249,9 @@ class _Lowerer:
         tail, bn, relu = self._bn_relu_tail(node)
         n, h, w, cin = x.shape
         cin_model = cin
-        if x.nchw_input and self.act_dtype == "bf16" and cin % 8 and not lz.relu and lz.sub is None:
-            # bf16 stem over the fp32 NCHW image: read a zero-padded NHWC bf16 copy
-            # instead (one 16-byte gather per tap), weights padded to match
+        if x.nchw_input and cin % (8 if self.act_dtype == "bf16" else 4) and not lz.relu and lz.sub is None:
+            # stem over the fp32 NCHW image: read a zero-padded NHWC copy in the
+            # activation dtype instead (one 16-byte gather per tap), weights padded to match
             x = self._packed_input(x)
             cin = x.shape[3]
         r, s = conv.kernel_size
@@ -285,13 +285,14 @@ class _Lowerer:
         self.env[tail] = out
 
     def _packed_input(self, x: Tensor) -> Tensor:
-        """The NHWC bf16, 8-channel-padded copy of the NCHW graph image (one PACK_INPUT op)."""
+        """The NHWC copy of the NCHW graph image in the activation dtype, channels padded to a 16-byte vector (one PACK_INPUT op)."""
         if getattr(self, "_packed", None) is None:
             n, h, w, c = x.shape
-            cp = (c + 7) // 8 * 8
-            out = self.new_tensor((n, h, w, cp), dtype="bf16")
+            v = 8 if self.act_dtype == "bf16" else 4
+            cp = (c + v - 1) // v * v
+            out = self.new_tensor((n, h, w, cp))
             self.emit(LoweredOp(PACK_INPUT, "copy", OpClass.MEMORY, dict(N=n, H=h, W=w, C=c, Cp=cp), [x], out,
-                                bytes_min=4 * n * h * w * c + 2 * n * h * w * cp, label="pack_input"))
+                                bytes_min=4 * n * h * w * c + self.esize * n * h * w * cp, label="pack_input"))
             self._packed = out
         return self._packed
 
