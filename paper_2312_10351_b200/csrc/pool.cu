@@ -28,12 +28,48 @@ template <typename T> __device__ __forceinline__ T from_f(float x);
 template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
 template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 
-// V-wide vector of T (V = 4: 16 B for fp32, 8 B for bf16)
+// V-wide vector of T: 16 B for fp32 x4 and bf16 x8, 8 B for bf16 x4
 template <typename T, int V> struct Vec;
 template <> struct Vec<float, 4> { using type = float4; };
 template <> struct Vec<__nv_bfloat16, 4> { using type = uint2; };
+template <> struct Vec<__nv_bfloat16, 8> { using type = uint4; };
 
-template <bool kMax, int V, typename T>
+template <typename T, int V>
+__device__ __forceinline__ void load_v(const T* src, float* x) {
+  if constexpr (V == 1) {
+    x[0] = to_f(*src);
+  } else {
+    const typename Vec<T, V>::type t = __ldg(reinterpret_cast<const typename Vec<T, V>::type*>(src));
+    const T* e = reinterpret_cast<const T*>(&t);
+#pragma unroll
+    for (int v = 0; v < V; ++v) x[v] = to_f(e[v]);
+  }
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void store_v(T* dst, const float* acc) {
+  if constexpr (V == 1) {
+    *dst = from_f<T>(acc[0]);
+  } else {
+    typename Vec<T, V>::type t;
+    T* e = reinterpret_cast<T*>(&t);
+#pragma unroll
+    for (int v = 0; v < V; ++v) e[v] = from_f<T>(acc[v]);
+    *reinterpret_cast<typename Vec<T, V>::type*>(dst) = t;
+  }
+}
+
+template <bool kMax>
+__device__ __forceinline__ float pool_acc(float acc, float x) {
+  // max: NaN propagates like torch (x > acc || isnan(x))
+  if constexpr (kMax) return (x > acc || isnan(x)) ? x : acc;
+  return acc + x;
+}
+
+// KS > 0: the window is KS x KS and every tap's load is issued before the
+// first reduction (all KS*KS loads in flight: the kernel is a single
+// memory round trip instead of KS*KS dependent ones); KS == 0: any window.
+template <bool kMax, int V, typename T, int KS>
 __global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long long* trace) {
   const T* in = static_cast<const T*>(a.in);
   T* outp = static_cast<T*>(a.out);
@@ -52,53 +88,49 @@ __global__ void __launch_bounds__(256) pool2d_nhwc(PoolArgs a, unsigned long lon
     int hs = oh * a.sh - a.ph, ws = ow * a.sw - a.pw;
     int he = min(hs + a.kh, a.H + a.ph), we = min(ws + a.kw, a.W + a.pw);
     const int pool_size = (he - hs) * (we - ws);
-    hs = max(hs, 0);
-    ws = max(ws, 0);
-    he = min(he, a.H);
-    we = min(we, a.W);
     float acc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[v] = kMax ? -INFINITY : 0.f;
-    for (int ih = hs; ih < he; ++ih) {
-      for (int iw = ws; iw < we; ++iw) {
-        const T* src = in + (static_cast<int64_t>(b * a.H + ih) * a.W + iw) * a.in_cs + a.in_coff + c;
-        float x[V];
-        if constexpr (V == 4) {
-          const typename Vec<T, 4>::type t = *reinterpret_cast<const typename Vec<T, 4>::type*>(src);
-          const T* e = reinterpret_cast<const T*>(&t);
+    const T* base = in + static_cast<int64_t>(b) * a.H * a.W * a.in_cs + a.in_coff + c;
+    int cnt;
+    if constexpr (KS > 0) {
+      float x[KS * KS][V];
+      bool ok[KS * KS];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) x[v] = to_f(e[v]);
-        } else {
+      for (int t = 0; t < KS * KS; ++t) {
+        const int ih = hs + t / KS, iw = ws + t % KS;
+        ok[t] = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+        if (ok[t]) load_v<T, V>(base + (static_cast<int64_t>(ih) * a.W + iw) * a.in_cs, x[t]);
+      }
+      cnt = 0;
 #pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = to_f(src[v]);
-        }
+      for (int t = 0; t < KS * KS; ++t) {
+        if (!ok[t]) continue;
+        ++cnt;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          if constexpr (kMax) {
-            // NaN propagates like torch (x > acc || isnan(x))
-            acc[v] = (x[v] > acc[v] || isnan(x[v])) ? x[v] : acc[v];
-          } else {
-            acc[v] += x[v];
-          }
+        for (int v = 0; v < V; ++v) acc[v] = pool_acc<kMax>(acc[v], x[t][v]);
+      }
+    } else {
+      hs = max(hs, 0);
+      ws = max(ws, 0);
+      he = min(he, a.H);
+      we = min(we, a.W);
+      cnt = (he - hs) * (we - ws);
+      for (int ih = hs; ih < he; ++ih) {
+        for (int iw = ws; iw < we; ++iw) {
+          float x[V];
+          load_v<T, V>(base + (static_cast<int64_t>(ih) * a.W + iw) * a.in_cs, x);
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[v] = pool_acc<kMax>(acc[v], x[v]);
         }
       }
     }
     if constexpr (!kMax) {
-      const int div = a.include_pad ? pool_size : (he - hs) * (we - ws);
+      const int div = a.include_pad ? pool_size : cnt;
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[v] = acc[v] / static_cast<float>(div);
     }
-    T* dst = outp + q * a.out_cs + a.out_coff + c;
-    if constexpr (V == 4) {
-      typename Vec<T, 4>::type t;
-      T* e = reinterpret_cast<T*>(&t);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) e[v] = from_f<T>(acc[v]);
-      *reinterpret_cast<typename Vec<T, 4>::type*>(dst) = t;
-    } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) dst[v] = from_f<T>(acc[v]);
-    }
+    store_v<T, V>(outp + q * a.out_cs + a.out_coff + c, acc);
   }
   trace_end(trace);
 }
@@ -172,23 +204,26 @@ opara_status launch_pool2d(const opara_op& op, cudaStream_t s, unsigned long lon
   a.ph = (int)op.i[14]; a.pw = (int)op.i[15]; a.include_pad = (int)op.i[16];
   const bool bf = op.i[18] == 1;
   const bool is_max = op.kind == OPARA_OP_MAXPOOL2D;
-  const bool vec = (a.C % 4 == 0) && (a.in_cs % 4 == 0) && (a.in_coff % 4 == 0) &&
-                   (a.out_cs % 4 == 0) && (a.out_coff % 4 == 0) &&
-                   (reinterpret_cast<uintptr_t>(a.in) % (bf ? 8 : 16) == 0) &&
-                   (reinterpret_cast<uintptr_t>(a.out) % (bf ? 8 : 16) == 0);
-  const int V = vec ? 4 : 1;
+  auto aligned = [&](int v, int bytes) {
+    return a.C % v == 0 && a.in_cs % v == 0 && a.in_coff % v == 0 && a.out_cs % v == 0 && a.out_coff % v == 0 &&
+           reinterpret_cast<uintptr_t>(a.in) % bytes == 0 && reinterpret_cast<uintptr_t>(a.out) % bytes == 0;
+  };
+  // vector width: 16 B per load where the channel views allow it
+  const int V = bf && aligned(8, 16) ? 8 : aligned(4, bf ? 8 : 16) ? 4 : 1;
+  const bool k3 = a.kh == 3 && a.kw == 3;
   const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
   LaunchCfg c;
-  static const void* table[2][2][2] = {
-      {{reinterpret_cast<const void*>(&pool2d_nhwc<false, 1, float>),
-        reinterpret_cast<const void*>(&pool2d_nhwc<false, 4, float>)},
-       {reinterpret_cast<const void*>(&pool2d_nhwc<true, 1, float>),
-        reinterpret_cast<const void*>(&pool2d_nhwc<true, 4, float>)}},
-      {{reinterpret_cast<const void*>(&pool2d_nhwc<false, 1, __nv_bfloat16>),
-        reinterpret_cast<const void*>(&pool2d_nhwc<false, 4, __nv_bfloat16>)},
-       {reinterpret_cast<const void*>(&pool2d_nhwc<true, 1, __nv_bfloat16>),
-        reinterpret_cast<const void*>(&pool2d_nhwc<true, 4, __nv_bfloat16>)}}};
-  c.func = table[bf ? 1 : 0][is_max ? 1 : 0][vec ? 1 : 0];
+#define OPARA_POOL_PICK(T, VV)                                                                          \
+  (is_max ? (k3 ? reinterpret_cast<const void*>(&pool2d_nhwc<true, VV, T, 3>)                          \
+                : reinterpret_cast<const void*>(&pool2d_nhwc<true, VV, T, 0>))                         \
+          : (k3 ? reinterpret_cast<const void*>(&pool2d_nhwc<false, VV, T, 3>)                         \
+                : reinterpret_cast<const void*>(&pool2d_nhwc<false, VV, T, 0>)))
+  if (bf)
+    c.func = V == 8 ? OPARA_POOL_PICK(__nv_bfloat16, 8) : V == 4 ? OPARA_POOL_PICK(__nv_bfloat16, 4)
+                                                                 : OPARA_POOL_PICK(__nv_bfloat16, 1);
+  else
+    c.func = V == 4 ? OPARA_POOL_PICK(float, 4) : OPARA_POOL_PICK(float, 1);
+#undef OPARA_POOL_PICK
   c.block = dim3(256);
   c.grid = dim3(std::max(1u, std::min<unsigned>(ceil_div(work, 256), 148u * 4u)));
   if (cfg) *cfg = c;

@@ -151,3 +151,46 @@ def test_attention_and_layernorm_rows():
     with torch.no_grad():
         ref = m.double()(ids)
     assert _rel(y.float().reshape(ref.shape).cpu(), ref) < 1e-2
+
+
+class PoolNet(nn.Module):
+    """Stem conv -> the pool under test, with a second conv on a channel
+    view so the pool also reads at a channel offset."""
+
+    def __init__(self, c, pool):
+        super().__init__()
+        self.stem = ConvBnRelu(3, c, 3, 1, 1)
+        self.pool = pool
+
+    def forward(self, x):
+        return self.pool(self.stem(x))
+
+
+POOL_CASES = [
+    ("max3s2ceil", lambda: nn.MaxPool2d(3, 2, ceil_mode=True)),
+    ("max3s2", lambda: nn.MaxPool2d(3, 2)),
+    ("max3s1p1", lambda: nn.MaxPool2d(3, 1, padding=1)),
+    ("max2s2", lambda: nn.MaxPool2d(2, 2)),
+    ("avg3s1p1", lambda: nn.AvgPool2d(3, 1, padding=1)),
+    ("avg3s1p1_nopad", lambda: nn.AvgPool2d(3, 1, padding=1, count_include_pad=False)),
+    ("avg3s2ceil", lambda: nn.AvgPool2d(3, 2, padding=1, ceil_mode=True, count_include_pad=False)),
+    ("avg5s3", lambda: nn.AvgPool2d(5, 3)),
+]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("c", [64, 36, 30])
+@pytest.mark.parametrize("name,make", POOL_CASES, ids=[c[0] for c in POOL_CASES])
+def test_pool_matches_torch(name, make, c, dtype):
+    """Every pooling path (3x3 all-taps-in-flight and generic windows; 16-,
+    8-byte and scalar channel vectors) against torch on the same stem output."""
+    from paper_2312_10351_b200 import engine
+    torch.manual_seed(1)
+    m = PoolNet(c, make()).eval()
+    x = torch.randn(1, 3, 23, 23)
+    sg = engine.compile(m, x, device=0, profile_reps=2, dtype=dtype)
+    y = sg.run(x.cuda()).float().permute(0, 3, 1, 2).cpu()   # executor activations are NHWC
+    with torch.no_grad():
+        ref = m.double()(x.double()).float()
+    assert y.shape == ref.shape
+    assert _rel(y, ref) < (1e-2 if dtype == "bf16" else 1e-5), name
