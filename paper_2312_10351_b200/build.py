@@ -12,6 +12,7 @@ dominant_share, see csrc/sched.cpp).
 from __future__ import annotations
 
 import argparse
+import hashlib
 import os
 import shutil
 import subprocess
@@ -22,13 +23,15 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = ROOT / "build" / "opara"
+_FLAGS = os.environ.get("OPARA_NVCC_FLAGS", "")  # A/B experiments only: own object dir + relink
+BUILD = ROOT / "build" / ("opara" if not _FLAGS else "opara-" + hashlib.sha1(_FLAGS.encode()).hexdigest()[:8])
 LIB = PKG / "libopara.so"
+STAMP = BUILD.parent / "libopara.flags"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", f"-I{ROOT / 'include'}", f"-I{CSRC}",
           "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math", "--expt-relaxed-constexpr",
-          *os.environ.get("OPARA_NVCC_FLAGS", "").split()]  # A/B experiments only
+          *_FLAGS.split()]
 
 
 def _sources() -> list[Path]:
@@ -64,7 +67,8 @@ def build(verbose: bool = False, clean: bool = False) -> Path:
     srcs = _sources()
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as pool:
         objs = list(pool.map(lambda s: _compile(s, verbose), srcs))
-    if LIB.exists() and LIB.stat().st_mtime >= max(o.stat().st_mtime for o in objs):
+    same_flags = STAMP.exists() and STAMP.read_text() == _FLAGS
+    if same_flags and LIB.exists() and LIB.stat().st_mtime >= max(o.stat().st_mtime for o in objs):
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcuda"]
@@ -72,6 +76,7 @@ def build(verbose: bool = False, clean: bool = False) -> Path:
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
     os.replace(tmp, LIB)
+    STAMP.write_text(_FLAGS)
     return LIB
 
 

@@ -33,6 +33,37 @@
 namespace opara {
 namespace {
 
+// Diagnostic build only (-DOPARA_PHASE_PROBE): CTA (0,0,0) of every launch
+// records %globaltimer at entry, after griddepcontrol.wait, first / last MMA
+// issue, accumulator ready and exit, read back by opara_debug_phase_read.
+#ifdef OPARA_PHASE_PROBE
+__device__ unsigned long long g_phase[4096][12];
+__device__ unsigned g_phase_n;
+#define PHASE(k)                                                              \
+  do {                                                                        \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ph[k] = global_ns(); \
+  } while (0)
+#define PHASE_FLUSH()                                                                               \
+  do {                                                                                              \
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {                        \
+      ph[7] = global_ns();                                                                          \
+      const unsigned slot = atomicAdd(&g_phase_n, 1u) & 4095u;                                      \
+      for (int q = 0; q < 8; ++q) g_phase[slot][q] = ph[q];                                         \
+      g_phase[slot][10] = ph[8];                                                                    \
+      g_phase[slot][11] = ph[9];                                                                    \
+      g_phase[slot][8] = (static_cast<unsigned long long>(a.M) << 40) | (static_cast<unsigned long long>(a.Cout) << 20) | a.K; \
+      g_phase[slot][9] = (static_cast<unsigned long long>(gridDim.x * gridDim.y * gridDim.z) << 32) | (static_cast<unsigned long long>(BN) << 24) | (nkb << 8) | (a.push ? 0x80 : 0) | (a.ws ? 0x40 : 0) | a.splits; \
+    }                                                                                               \
+  } while (0)
+#else
+#define PHASE(k) \
+  do {           \
+  } while (0)
+#define PHASE_FLUSH() \
+  do {                \
+  } while (0)
+#endif
+
 constexpr int kBK = 32;                     // bf16 k elements per stage (64 B rows)
 constexpr int kGatherWarps = 4;
 constexpr int kLoadWarp = 4, kMmaWarp = 5;
@@ -113,6 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   constexpr uint32_t kIdesc = tc::instr_desc(1, 128, BN);
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
   static_assert(BN * 128 * 4 <= kStages * kStage, "epilogue tile must fit in the pipeline smem");
+  static_assert(48 * 1024 <= kStages * kStage, "push staging blocks must fit in the pipeline smem");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -122,7 +154,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   uint32_t* tslot = reinterpret_cast<uint32_t*>(accum + 1);
 
   pdl_trigger();
+#ifdef OPARA_PHASE_PROBE
+  __shared__ unsigned long long ph[10];
+  if (threadIdx.x < 10) ph[threadIdx.x] = 0;
+#endif
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) PHASE(0);
   const int n0 = blockIdx.x * BN;
   const int mt = blockIdx.y;
   const int kb0 = blockIdx.z * a.kb_per_split;
@@ -138,6 +175,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       if (ch + e < a.Cout) bias[e] = __ldg(a.bias + ch + e);
   }
 #endif
+  // the push epilogue's owner reduction: thread = output channel
+  const float push_bias = (a.push && a.bias && tid < 128 && mt * 128 + tid < a.Cout) ? __ldg(a.bias + mt * 128 + tid) : 0.f;
 
   // push-mode split-K: receive buffer [src rank][128 channels][rows_per columns]
   // fp32 behind the ring (other CTAs may push while this CTA's ring is busy)
@@ -153,16 +192,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     if (push) tc::mbar_init(rbar, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 0) tc::tmem_alloc(tslot, kTmemCols);
+  constexpr int kTmemWarp = kMmaWarp;   // the MMA warp is idle in every epilogue: it frees TMEM off the critical path
+  if (warp == kTmemWarp) tc::tmem_alloc(tslot, kTmemCols);   // (and frees them: an epilogue-idle warp)
   tc::tc_fence_before();
   if (push) {
     // every CTA's receive barrier is initialised before anyone pushes (this
     // runs before griddepcontrol.wait, overlapping the predecessor kernel)
     tc::cluster_sync();
     if (tid == 0) {
+      // every rank bulk-copies one whole [128][rows_per] block to each owner
       const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
-      const int mine = max(0, min(BN, r0 + a.rows_per) - r0);
-      tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * mine * 128 * 4));
+      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4));
     }
   } else {
     __syncthreads();
@@ -195,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     }
     pdl_wait();
     trace_begin(trace);
+    if (tid == 0) PHASE(1);
     // Fused input ReLU (relu_in): the copies of stage i are committed as one
     // cp.async group; once stage i-1's group has landed this thread clamps
     // its own chunks of it in place (bf16 max with 0), fences them into the
@@ -385,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       const int s = i % kStages;
       tc::mbar_wait(&full[s], (i / kStages) & 1);
       tc::tc_fence_after();
+      if (i == 0) PHASE(2);
       const uint32_t base = tc::smem_u32(smem + s * kStage);
 #pragma unroll
       for (int ks = 0; ks < kBK / 16; ++ks) {
@@ -394,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       }
       tc::mma_commit(&empty[s]);
     }
+    PHASE(3);
     tc::mma_commit(accum);
   }
   __syncwarp();
@@ -413,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     if (warp < 4) {
       tc::mbar_wait(accum, 0);
       tc::tc_fence_after();
+      if (tid == 0) PHASE(4);
       const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
       const float b = (a.bias && ch_ok) ? __ldg(a.bias + ch) : 0.f;
 #pragma unroll
@@ -437,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
+    if (warp == kTmemWarp) {
       tc::tc_fence_after();
       tc::tmem_dealloc(tmem, kTmemCols);
     }
@@ -483,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       }
     }
     tc::cluster_sync();   // peers may still be reading this CTA's channel sums
+    PHASE_FLUSH();
     trace_end(trace);
     return;
   }
@@ -496,6 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     if (warp < 4) {
       tc::mbar_wait(accum, 0);
       tc::tc_fence_after();
+      if (tid == 0) PHASE(4);
       const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
       float* mine = a.ws + (static_cast<int64_t>(blockIdx.z) * tiles + tile) * plane + warp * 32 + lane;
 #pragma unroll 4
@@ -508,12 +554,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
+    if (warp == kTmemWarp) {
       tc::tc_fence_after();
       tc::tmem_dealloc(tmem, kTmemCols);
     }
     if (!splitk_arrive_last(a.cnt + tile, a.splits)) {
-      trace_end(trace);
+      PHASE_FLUSH();
+    trace_end(trace);
       return;
     }
     TO* out = static_cast<TO*>(a.out);
@@ -538,73 +585,89 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
         }
       }
     }
+    PHASE_FLUSH();
     trace_end(trace);
     return;
   }
   if (push) {
-    // TMEM -> registers -> st.async of 4-column float4 groups straight into the
-    // owning rank's receive buffer (slot = my rank); the owner's mbarrier
-    // counts the bytes.  No cluster barrier and no remote loads on this path.
+    // TMEM -> registers -> this CTA's smem (the drained ring), laid out as one
+    // contiguous [128 channels][rows_per] block per owning rank; then one
+    // thread bulk-copies each block into its owner's receive slot (TMA engine,
+    // complete_tx on the owner's mbarrier).  No cluster barrier, no remote loads.
     const uint32_t me = tc::cluster_ctarank();
     const int rp = a.rows_per;
+    float* stage = reinterpret_cast<float*>(smem);
     if (warp < 4) {
       tc::mbar_wait(accum, 0);
       tc::tc_fence_after();
+      if (tid == 0) PHASE(4);
       const int chl = warp * 32 + lane;
       const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-      const uint32_t recv_s = tc::smem_u32(recv);
-      const uint32_t rbar_s = tc::smem_u32(rbar);
 #pragma unroll 2
       for (int c8 = 0; c8 < BN / 8; ++c8) {
         float v[8];
         tc::tmem_ld8(trow + c8 * 8, v);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = c8 * 8 + h * 4;
-          const uint32_t owner = static_cast<uint32_t>(col / rp);
-          const uint32_t off = static_cast<uint32_t>(((me * 128 + chl) * rp + (col - owner * rp)) * 4);
-          tc::st_async_f4(tc::map_cluster(recv_s + off, owner), make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2],
-                                                                            v[4 * h + 3]),
-                          tc::map_cluster(rbar_s, owner));
+        for (int e = 0; e < 8; ++e) {   // block = [owner][rows_per cols][128 ch]: lanes write consecutive words
+          const int col = c8 * 8 + e;
+          const int owner = col / rp;
+          stage[(owner * rp + (col - owner * rp)) * 128 + chl] = v[e];
         }
       }
+      tc::fence_proxy_async_smem();   // generic-proxy writes -> the bulk copy engine
+      if (tid == 0) PHASE(8);
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
+    if (tid == 0) {
+      PHASE(9);
+      const uint32_t block = static_cast<uint32_t>(128 * rp * 4);
+      const uint32_t rbar_s = tc::smem_u32(rbar), recv_s = tc::smem_u32(recv), stage_s = tc::smem_u32(stage);
+      for (int o = 0; o < a.splits && o * rp < BN; ++o)
+        tc::bulk_s2cluster(tc::map_cluster(recv_s + me * block, o), stage_s + o * block, block,
+                           tc::map_cluster(rbar_s, o));
+      tc::bulk_commit();
+    }
+    if (warp == kTmemWarp) {
       tc::tc_fence_after();
       tc::tmem_dealloc(tmem, kTmemCols);
     }
-    // owner: wait for every rank's partial columns, reduce in rank order
+    // owner: wait for every rank's block, reduce in rank order (thread = channel)
     const int r0 = static_cast<int>(me) * rp;
     const int mine = max(0, min(BN, r0 + rp) - r0);
-    if (mine > 0) {
+    if (mine > 0 && tid < 128) {
       tc::mbar_wait_cluster(rbar, 0);
+      if (tid == 0) PHASE(5);
+      if (tid == 0) PHASE(6);
       TO* out = static_cast<TO*>(a.out);
-      const int groups = mine / 4;
-      for (int t = tid; t < 128 * groups; t += kThreads) {
-        const int chl = t & 127, g = t >> 7;
-        const int ch = mt * 128 + chl;
-        if (ch >= a.Cout) continue;
-        float4 acc = *reinterpret_cast<const float4*>(recv + (0 * 128 + chl) * rp + 4 * g);
-        for (int z = 1; z < a.splits; ++z) {
-          const float4 q = *reinterpret_cast<const float4*>(recv + (z * 128 + chl) * rp + 4 * g);
-          acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
-        }
-        const float b = a.bias ? __ldg(a.bias + ch) : 0.f;
-        const float y[4] = {act_fn(acc.x + b, a.act), act_fn(acc.y + b, a.act), act_fn(acc.z + b, a.act),
-                            act_fn(acc.w + b, a.act)};
+      const int chl = tid, ch = mt * 128 + chl;
+      if (ch < a.Cout) {
+        for (int c0 = 0; c0 < mine; c0 += 4) {   // recv = [src rank][rows_per cols][128 ch]
+          float part[kMaxSplits][4];               // every load of 4 columns issued before the adds
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int p = n0 + r0 + 4 * g + e;
-          if (p < a.M) {
-            TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
-            if constexpr (std::is_same<TO, float>::value) *dst = y[e];
-            else *dst = __float2bfloat16_rn(y[e]);
+          for (int z = 0; z < kMaxSplits; ++z)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (z < a.splits) part[z][e] = recv[(z * rp + c0 + e) * 128 + chl];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float acc = part[0][e];
+#pragma unroll
+            for (int z = 1; z < kMaxSplits; ++z)
+              if (z < a.splits) acc += part[z][e];
+            const int p = n0 + r0 + c0 + e;
+            if (p < a.M) {
+              TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
+              const float y = act_fn(acc + push_bias, a.act);
+              if constexpr (std::is_same<TO, float>::value) *dst = y;
+              else *dst = __float2bfloat16_rn(y);
+            }
           }
         }
       }
     }
+    if (tid == 0) tc::bulk_wait_read();   // the source blocks stay valid until the engine has read them
+    PHASE_FLUSH();
     trace_end(trace);
     return;
   }
@@ -612,6 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   if (warp < 4) {
     tc::mbar_wait(accum, 0);
     tc::tc_fence_after();
+    if (tid == 0) PHASE(4);
     const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
 #pragma unroll 4
     for (int c8 = 0; c8 < BN / 8; ++c8) {
@@ -620,6 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
 #pragma unroll
       for (int e = 0; e < 8; ++e) tile[(c8 * 8 + e) * 128 + warp * 32 + lane] = v[e];
     }
+    if (tid == 0) PHASE(8);
   }
   tc::tc_fence_before();
   const int splits = a.splits;
@@ -627,12 +692,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     tc::cluster_sync();
   else
     __syncthreads();
+  if (tid == 0) PHASE(9);
   // every TMEM read is done (the tile is in smem): free the columns now so a
   // PDL-launched successor CTA on this SM can allocate while we reduce
-  if (warp == 0) {
+  if (warp == kTmemWarp) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, kTmemCols);
   }
+  if (tid == 0) PHASE(5);
   const int rank = splits > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
   const int rows_per = (BN + splits - 1) / splits;
   const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
@@ -647,54 +714,67 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
 #endif
   const uint32_t tile_s = tc::smem_u32(tile);
   TO* out = static_cast<TO*>(a.out);
-  for (int row = r0 + warp; row < r1; row += kThreads / 32) {
-    const int p = n0 + row;
-    if (p >= a.M) break;
-    const uint32_t off = static_cast<uint32_t>((row * 128 + lane * 4) * 4);
-    float4 acc;
-    if (splits > 1) {
-      float4 part[kMaxSplits];
+  // a row per warp iteration, every split's DSMEM load issued before the first add
+  constexpr int kRB = 1, kWarps = kThreads / 32;   // (2 rows in flight measured slower: Inception 0.390 -> 0.402 ms)
+  for (int row0 = r0 + warp; row0 < r1; row0 += kRB * kWarps) {
+    float4 part[kRB][kMaxSplits];
+    bool ok[kRB];
 #pragma unroll
-      for (int z = 0; z < kMaxSplits; ++z)
-        if (z < splits) part[z] = tc::ld_dsmem_f4(tc::map_cluster(tile_s + off, z));
-      acc = part[0];
+    for (int rb = 0; rb < kRB; ++rb) {
+      const int row = row0 + rb * kWarps;
+      ok[rb] = row < r1 && n0 + row < a.M;
+      const uint32_t off = static_cast<uint32_t>((row * 128 + lane * 4) * 4);
+      if (!ok[rb]) continue;
+      if (splits > 1) {
+#pragma unroll
+        for (int z = 0; z < kMaxSplits; ++z)
+          if (z < splits) part[rb][z] = tc::ld_dsmem_f4(tc::map_cluster(tile_s + off, z));
+      } else {
+        part[rb][0] = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(tile) + off);
+      }
+    }
+#pragma unroll
+    for (int rb = 0; rb < kRB; ++rb) {
+      if (!ok[rb]) continue;
+      const int p = n0 + row0 + rb * kWarps;
+      float4 acc = part[rb][0];
 #pragma unroll
       for (int z = 1; z < kMaxSplits; ++z)
         if (z < splits) {
-          acc.x += part[z].x; acc.y += part[z].y; acc.z += part[z].z; acc.w += part[z].w;
+          acc.x += part[rb][z].x; acc.y += part[rb][z].y; acc.z += part[rb][z].z; acc.w += part[rb][z].w;
         }
-    } else {
-      acc = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(tile) + off);
-    }
-    float y[4] = {act_fn(acc.x + bias[0], a.act), act_fn(acc.y + bias[1], a.act),
-                  act_fn(acc.z + bias[2], a.act), act_fn(acc.w + bias[3], a.act)};
-    TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
-    if constexpr (std::is_same<TO, float>::value) {
-      if (a.vec_out && ch + 3 < a.Cout) {
-        *reinterpret_cast<float4*>(dst) = make_float4(y[0], y[1], y[2], y[3]);
-        continue;
+      float y[4] = {act_fn(acc.x + bias[0], a.act), act_fn(acc.y + bias[1], a.act),
+                    act_fn(acc.z + bias[2], a.act), act_fn(acc.w + bias[3], a.act)};
+      TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
+      if constexpr (std::is_same<TO, float>::value) {
+        if (a.vec_out && ch + 3 < a.Cout) {
+          *reinterpret_cast<float4*>(dst) = make_float4(y[0], y[1], y[2], y[3]);
+          continue;
+        }
+      } else {
+        if (a.vec_out && ch + 3 < a.Cout) {
+          __nv_bfloat162 lo2 = __floats2bfloat162_rn(y[0], y[1]);
+          __nv_bfloat162 hi2 = __floats2bfloat162_rn(y[2], y[3]);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo2);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi2);
+          *reinterpret_cast<uint2*>(dst) = pk;
+          continue;
+        }
       }
-    } else {
-      if (a.vec_out && ch + 3 < a.Cout) {
-        __nv_bfloat162 lo2 = __floats2bfloat162_rn(y[0], y[1]);
-        __nv_bfloat162 hi2 = __floats2bfloat162_rn(y[2], y[3]);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&lo2);
-        pk.y = *reinterpret_cast<uint32_t*>(&hi2);
-        *reinterpret_cast<uint2*>(dst) = pk;
-        continue;
-      }
-    }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (ch + e < a.Cout) {
-        if constexpr (std::is_same<TO, float>::value) dst[e] = y[e];
-        else dst[e] = __float2bfloat16_rn(y[e]);
+      for (int e = 0; e < 4; ++e) {
+        if (ch + e < a.Cout) {
+          if constexpr (std::is_same<TO, float>::value) dst[e] = y[e];
+          else dst[e] = __float2bfloat16_rn(y[e]);
+        }
       }
     }
   }
+  if (tid == 0) PHASE(6);
   if (splits > 1) tc::cluster_sync();  // peers may still be reading this CTA's tile
-  trace_end(trace);
+  PHASE_FLUSH();
+    trace_end(trace);
 }
 
 template <int BN>
@@ -932,3 +1012,17 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
 }
 
 }  // namespace opara
+
+#ifdef OPARA_PHASE_PROBE
+extern "C" int opara_debug_phase_read(unsigned long long* host, int max_records, int reset) {
+  unsigned n = 0;
+  cudaMemcpyFromSymbol(&n, opara::g_phase_n, sizeof(n));
+  const int k = static_cast<int>(std::min<unsigned>(n, std::min(max_records, 4096)));
+  if (k > 0) cudaMemcpyFromSymbol(host, opara::g_phase, sizeof(unsigned long long) * 12 * k);
+  if (reset) {
+    const unsigned z = 0;
+    cudaMemcpyToSymbol(opara::g_phase_n, &z, sizeof(z));
+  }
+  return k;
+}
+#endif

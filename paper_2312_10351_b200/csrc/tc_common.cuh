@@ -198,6 +198,19 @@ __device__ __forceinline__ void st_async_f4(uint32_t caddr, float4 v, uint32_t c
                : "memory");
 }
 
+// 1-D bulk copy of this CTA's shared memory into (possibly another CTA's)
+// shared memory of the cluster (TMA engine); bytes complete_tx on the
+// destination's mbarrier `cbar` (cluster address).  bytes % 16 == 0.
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst_caddr, uint32_t src_saddr, uint32_t bytes,
+                                               uint32_t cbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst_caddr), "r"(src_saddr), "r"(bytes), "r"(cbar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the issuing thread's bulk copies have finished READING their source
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 // Wait on a local mbarrier phase that remote st.async / bulk copies complete
 // (acquire at cluster scope so the remote bytes are visible).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {

@@ -811,7 +811,7 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
     Opara's bounded grids (each conv sized for its DAG level's share of the
     SMs, so concurrent branches co-reside); "auto" = build every combination
     of {full, bounded} grids x {push, pull, auto} split-K reductions (and,
-    when bounded wins, SM-share scales 0.75 / 1.5 / 2), replay each Opara
+    for the fastest bounded one, SM-share scales 0.75 / 1.5 / 2), replay each Opara
     graph and keep the fastest (all latencies are kept in ``autotune``).  tune: pick every tensor-core
     conv/GEMM's tile width and split-K by measurement (ScheduledGraph._autotune).
     splitk: split-K reduction ("push" / "pull" / "auto", see ScheduledGraph) for
@@ -843,10 +843,11 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
     for bounded in (False, True):
         for splitk in ("push", "pull", "auto"):
             trial(bounded, splitk)
-    if best[0].bound_grids:   # refine the SM shares of the winning bounded variant
-        splitk = best[0].splitk
-        for scale in (0.75, 1.5, 2.0):
-            trial(True, splitk, scale)
+    # refine the SM shares of the fastest bounded variant (even when a full-grid
+    # variant leads: a larger share often overtakes it)
+    splitk = min((t for t in tried if t["bounded"]), key=lambda t: t["parallel_ms"])["splitk"]
+    for scale in (0.75, 1.5, 2.0):
+        trial(True, splitk, scale)
     sg = best[0]
     sg.autotune = tried
     return sg
