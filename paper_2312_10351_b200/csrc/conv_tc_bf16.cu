@@ -69,6 +69,9 @@ constexpr int kGatherWarps = 4;
 constexpr int kLoadWarp = 4, kMmaWarp = 5;
 constexpr int kThreads = 192;
 constexpr int kMaxSplits = 8;
+#ifndef OPARA_PUSH_MAX_KB
+#define OPARA_PUSH_MAX_KB 48   // split-K push receive buffer limit (KB of smem beyond the ring)
+#endif
 constexpr uint32_t kWBytes = 128 * kBK * 2;  // 8 KB
 
 // Ring depth per tile width.  The 16-wide tile keeps a 24-deep ring (216 KB):
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   constexpr uint32_t kIdesc = tc::instr_desc(1, 128, BN);
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
   static_assert(BN * 128 * 4 <= kStages * kStage, "epilogue tile must fit in the pipeline smem");
-  static_assert(48 * 1024 <= kStages * kStage, "push staging blocks must fit in the pipeline smem");
+  static_assert(OPARA_PUSH_MAX_KB * 1024 <= kStages * kStage, "push staging blocks must fit in the pipeline smem");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -811,7 +814,7 @@ const BfVariant* bf_variants() {
   return v;
 }
 
-constexpr size_t kPushMaxBytes = 48 * 1024;
+constexpr size_t kPushMaxBytes = OPARA_PUSH_MAX_KB * 1024;
 constexpr size_t kSmemLimit = 232448 - 1024;   // 227 KB opt-in smem per CTA, minus static smem headroom
 inline size_t attr_smem(size_t ring) { return std::min(ring + kPushMaxBytes, kSmemLimit); }
 

@@ -161,21 +161,42 @@ def concurrent_convs(program: Program) -> dict[int, int]:
     return {v: count[level[v]] for v, op in enumerate(program.ops) if op.kind == CONV2D}
 
 
+def serial_ops(program: Program) -> set[int]:
+    """Ops that can never run beside another op: every other op is an ancestor
+    or a descendant (the DAG's articulation points in execution order)."""
+    n = len(program.ops)
+    succs = [[] for _ in range(n)]
+    for u, v in program.edges:
+        succs[u].append(v)
+    desc = [0] * n                      # bitset of descendants (ops are topologically ordered)
+    for v in range(n - 1, -1, -1):
+        for w in succs[v]:
+            desc[v] |= desc[w] | (1 << w)
+    anc = [0] * n
+    for v in range(n):
+        for w in succs[v]:
+            anc[w] |= anc[v] | (1 << v)
+    full = (1 << n) - 1
+    return {v for v in range(n) if (anc[v] | desc[v] | (1 << v)) == full}
+
+
 def concurrency_targets(program: Program, num_sms: int = 148, scale: float = 1.0) -> dict[int, int]:
     """CTA budget per conv: the SMs are shared among the convs of the same DAG
     level (longest-path depth) in proportion to their FLOPs, so branches that
     can run concurrently are sized to co-reside instead of each claiming the
     whole GPU (Opara's bounded grids).  `scale` oversubscribes
     (> 1) or undersubscribes (< 1) the shares; compile(bound_grids="auto")
-    searches it."""
+    searches it.  Ops that can never run beside another (serial_ops) keep the
+    full-GPU grid: there is nothing to co-reside with."""
     level = dag_levels(program)
+    serial = serial_ops(program)
     work: dict[int, int] = {}
     for v, op in enumerate(program.ops):
         if op.kind == CONV2D:
             work[level[v]] = work.get(level[v], 0) + op.flops
     out = {}
     for v, op in enumerate(program.ops):
-        if op.kind == CONV2D and work.get(level[v]):
+        if op.kind == CONV2D and work.get(level[v]) and v not in serial:
             out[v] = max(8, int(round(scale * num_sms * op.flops / work[level[v]])))
     return out
 

@@ -118,6 +118,21 @@ def test_concurrency_targets_share_levels():
     assert t and all(8 <= v <= 148 for v in t.values())
 
 
+def test_serial_ops_keep_full_grids():
+    """BERT: Q/K/V projections run beside each other and get SM shares; the
+    output projection and the FFN are alone in the DAG and keep full grids."""
+    m, _, ids = zoo.build_bert()
+    prog = frontend.lower(m, ids, "bf16")
+    serial, t = engine.serial_ops(prog), engine.concurrency_targets(prog)
+    convs = [v for v, o in enumerate(prog.ops) if o.kind == frontend.CONV2D]
+    assert len(t) == 36 and all(v not in serial for v in t)
+    assert sum(1 for v in convs if v in serial) == 37
+    assert all(t[v] == round(148 / 3) for v in t)
+    model, x = zoo.build("googlenet")
+    g = frontend.lower(model, x)
+    assert 0 in engine.serial_ops(g) and 1 in engine.serial_ops(g)   # PACK_INPUT -> stem conv
+
+
 def _workload(name):
     if name == "bert_base":
         m, _, ids = zoo.build_bert()
