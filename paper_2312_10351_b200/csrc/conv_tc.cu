@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   constexpr int kAcc = BN >= 256 ? 2 : 3;
   constexpr uint32_t kTmemCols = BN >= 256 ? 512 : (BN * 4 <= 32 ? 32 : BN * 4);
   static_assert(BN * 128 * 4 <= kStages * kStage, "epilogue tile must fit in the pipeline smem");
+  static_assert(48 * 1024 <= kStages * kStage, "push staging blocks must fit in the pipeline smem");
 
   // No-swizzle UMMA operands need 16-byte alignment only; indexing the extern
   // array directly keeps every access in the shared state space (LDS/STS).
@@ -135,6 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     if (ch + 3 < a.Cout) bias4.w = __ldg(a.bias + ch + 3);
   }
 #endif
+  // push-epilogue owner reduction: thread = output channel
+  const float push_bias = (a.push && a.bias && tid < 128 && mt * 128 + tid < a.Cout) ? __ldg(a.bias + mt * 128 + tid) : 0.f;
 
   // push-mode split-K receive buffer [src rank][128 channels][rows_per] fp32, behind the ring
   uint64_t* rbar = accum + 2;
@@ -150,14 +153,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     if (push) tc::mbar_init(rbar, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 0) tc::tmem_alloc(tslot, kTmemCols);
+  // TMEM is allocated and freed by the MMA warp: idle in every epilogue
+  if (warp == kMmaWarp) tc::tmem_alloc(tslot, kTmemCols);
   tc::tc_fence_before();
   if (push) {   // receive barriers initialised cluster-wide before anyone pushes
     tc::cluster_sync();
-    if (tid == 0) {
+    if (tid == 0) {   // every rank bulk-copies one whole [rows_per][128] block to each owner
       const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
-      const int mine = max(0, min(BN, r0 + a.rows_per) - r0);
-      tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * mine * 128 * 4));
+      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4));
     }
   } else {
     __syncthreads();
@@ -335,17 +338,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   // smem reads by the tensor core, are complete once `accum` fires).
   DBG(3);
   if (push) {
-    // TMEM -> registers (sum of the 3xTF32 accumulators) -> st.async of 4-column
-    // float4 groups into the owning rank's receive buffer; owners reduce in rank order
+    // TMEM -> registers (sum of the 3xTF32 accumulators) -> this CTA's idle ring
+    // smem as one contiguous [rows_per cols][128 ch] block per owning rank;
+    // one thread bulk-copies each block into its owner's receive slot (TMA
+    // engine, complete_tx on the owner's mbarrier); owners reduce in rank order.
     const uint32_t me = tc::cluster_ctarank();
     const int rp = a.rows_per;
+    float* stage = reinterpret_cast<float*>(smem);
     if (warp < kProducerWarps) {
       tc::mbar_wait(accum, 0);
       tc::tc_fence_after();
       const int quarter = warp & 3, half = warp >> 2;
       const int chl = quarter * 32 + lane;
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-      const uint32_t recv_s = tc::smem_u32(recv), rbar_s = tc::smem_u32(rbar);
       constexpr int kC8 = BN / 8 / (kProducerWarps / 4);
 #pragma unroll 2
       for (int c8 = half * kC8; c8 < (half + 1) * kC8; ++c8) {
@@ -354,48 +359,51 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
         tc::tmem_ld8(trow + BN + c8 * 8, c1);
         if constexpr (kAcc == 3) tc::tmem_ld8(trow + 2 * BN + c8 * 8, c2);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] += kAcc == 3 ? (c1[e] + c2[e]) : c1[e];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = c8 * 8 + h * 4;
-          const uint32_t owner = static_cast<uint32_t>(col / rp);
-          const uint32_t off = static_cast<uint32_t>(((me * 128 + chl) * rp + (col - owner * rp)) * 4);
-          tc::st_async_f4(tc::map_cluster(recv_s + off, owner),
-                          make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]),
-                          tc::map_cluster(rbar_s, owner));
+        for (int e = 0; e < 8; ++e) {
+          const int col = c8 * 8 + e, owner = col / rp;
+          stage[(owner * rp + (col - owner * rp)) * 128 + chl] = v[e] + (kAcc == 3 ? (c1[e] + c2[e]) : c1[e]);
         }
       }
+      tc::fence_proxy_async_smem();   // generic-proxy writes -> the bulk copy engine
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
+    if (tid == 0) {
+      const uint32_t block = static_cast<uint32_t>(128 * rp * 4);
+      const uint32_t rbar_s = tc::smem_u32(rbar), recv_s = tc::smem_u32(recv), stage_s = tc::smem_u32(stage);
+      for (int o = 0; o < a.splits && o * rp < BN; ++o)
+        tc::bulk_s2cluster(tc::map_cluster(recv_s + me * block, o), stage_s + o * block, block,
+                           tc::map_cluster(rbar_s, o));
+      tc::bulk_commit();
+    }
+    if (warp == kMmaWarp) {
       tc::tc_fence_after();
       tc::tmem_dealloc(tmem, kTmemCols);
     }
     const int r0 = static_cast<int>(me) * rp;
     const int mine = max(0, min(BN, r0 + rp) - r0);
-    if (mine > 0) {
+    const int ch = mt * 128 + tid;
+    if (mine > 0 && tid < 128 && ch < a.Cout) {
       tc::mbar_wait_cluster(rbar, 0);
-      const int groups = mine / 4;
-      for (int t = tid; t < 128 * groups; t += kThreads) {
-        const int chl = t & 127, g = t >> 7;
-        const int ch = mt * 128 + chl;
-        if (ch >= a.Cout) continue;
-        float4 acc = *reinterpret_cast<const float4*>(recv + chl * rp + 4 * g);
-        for (int z = 1; z < a.splits; ++z) {
-          const float4 q = *reinterpret_cast<const float4*>(recv + (z * 128 + chl) * rp + 4 * g);
-          acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
-        }
-        const float b = a.bias ? __ldg(a.bias + ch) : 0.f;
-        float y[4] = {acc.x + b, acc.y + b, acc.z + b, acc.w + b};
+      for (int c0 = 0; c0 < mine; c0 += 4) {   // recv = [src rank][rows_per cols][128 ch]
+        float part[kMaxSplits][4];               // every load of 4 columns issued before the adds
+#pragma unroll
+        for (int z = 0; z < kMaxSplits; ++z)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (z < a.splits) part[z][e] = recv[(z * rp + c0 + e) * 128 + tid];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          y[e] = apply_act(y[e], a.relu);
-          const int p = n0 + r0 + 4 * g + e;
-          if (p < a.M) a.out[static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch] = y[e];
+          float acc = part[0][e];
+#pragma unroll
+          for (int z = 1; z < kMaxSplits; ++z)
+            if (z < a.splits) acc += part[z][e];
+          const int p = n0 + r0 + c0 + e;
+          if (p < a.M) a.out[static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch] = apply_act(acc + push_bias, a.relu);
         }
       }
     }
+    if (tid == 0) tc::bulk_wait_read();   // the source blocks stay valid until the engine has read them
     trace_end(trace);
     return;
   }
@@ -432,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     __syncthreads();
   // every TMEM read is done (the tile is in smem): free the columns now so a
   // PDL-launched successor CTA on this SM can allocate while we reduce
-  if (warp == 0) {
+  if (warp == kMmaWarp) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, kTmemCols);
   }
