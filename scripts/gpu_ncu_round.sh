@@ -17,4 +17,10 @@ for spec in ${NCU_SPECS:-"inception_v3 f32 conv2d_tc_tf32x3|bert_base bf16 conv2
      -o gpurun_out/full_${m}_$dt python bench.py --model $m --dtype $dt --grids $g --steps 3 --warmup 3 \
      --cpu-seconds 0.1 --profile-reps 2 --profile-region > /dev/null 2>&1; echo "full rc=$?"
   timeout 300 python scripts/timeline.py $m $dt > /dev/null 2>&1; echo "timeline rc=$?"
+  # summarise here: the raw reports and launch CSVs exceed what gpurun brings back
+  mkdir -p gpurun_out/profiles
+  python scripts/summarize_ncu.py r01_${m}_$dt gpurun_out/launches_${m}_$dt.csv gpurun_out/full_${m}_$dt.ncu-rep \
+     gpurun_out/profiles > /dev/null 2>&1; echo "summary rc=$?"
+  mv gpurun_out/r01_${m}_${dt}_timeline.md gpurun_out/profiles/ 2>/dev/null
+  rm -f gpurun_out/launches_${m}_$dt.csv gpurun_out/full_${m}_$dt.ncu-rep gpurun_out/pre_$m.json
 done

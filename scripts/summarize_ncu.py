@@ -1,6 +1,9 @@
 """Summarise ncu outputs (launch list CSV + one --set full report) into profiles/.
 
-    python scripts/summarize_ncu.py <tag> <launches.csv> <full.ncu-rep>
+    python scripts/summarize_ncu.py <tag> <launches.csv> <full.ncu-rep> [outdir]
+
+(outdir defaults to profiles/; gpu_ncu_round.sh summarises on the GPU box into
+gpurun_out/profiles/ because the raw reports are too large to bring back.)
 """
 import collections
 import csv
@@ -9,7 +12,7 @@ import sys
 from pathlib import Path
 
 tag, launches, rep = sys.argv[1], Path(sys.argv[2]), Path(sys.argv[3])
-out = Path("profiles")
+out = Path(sys.argv[4] if len(sys.argv) > 4 else "profiles")
 out.mkdir(exist_ok=True)
 lines = []
 
