@@ -137,12 +137,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   }
 #endif
   // push-epilogue owner reduction: thread = output channel
-  const float push_bias = (a.push && a.bias && tid < 128 && mt * 128 + tid < a.Cout) ? __ldg(a.bias + mt * 128 + tid) : 0.f;
+  const float push_bias = ((a.push || a.splits > 1) && a.bias && tid < 128 && mt * 128 + tid < a.Cout) ? __ldg(a.bias + mt * 128 + tid) : 0.f;
 
   // push-mode split-K receive buffer [src rank][128 channels][rows_per] fp32, behind the ring
   uint64_t* rbar = accum + 2;
   float* recv = reinterpret_cast<float*>(smem + kStages * kStage + 512);
   const bool push = a.push != 0;
+  // Opt-in (-DOPARA_RING_PULL) pull-mode split-K without DSMEM loads: after one
+  // cluster barrier every rank bulk-copies its staged blocks into the owners'
+  // (now idle) rings.  Measured slower than the DSMEM pull in graphs
+  // (GoogLeNet fp32 0.234 -> 0.246 ms, BERT 0.482 -> 0.485 ms), so off by default.
+  const uint32_t stage_bytes = static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4);
+#ifndef OPARA_RING_PULL
+  const bool ring = false;
+#else
+  const bool ring = !push && a.splits > 1 && 2 * stage_bytes <= kStages * kStage;
+#endif
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], 32 * (kProducerWarps / 2) + 1);  // converters + the weight loader
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(accum, 1);
-    if (push) tc::mbar_init(rbar, 1);
+    if (push || ring) tc::mbar_init(rbar, 1);
     tc::fence_barrier_init();
   }
   // TMEM is allocated and freed by the MMA warp: idle in every epilogue
@@ -163,6 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4));
     }
   } else {
+    if (ring && tid == 0) {   // owners expect every rank's block (the epilogue's cluster barrier orders it)
+      const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
+      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, stage_bytes);
+    }
     __syncthreads();
   }
   tc::tc_fence_after();
@@ -337,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   // TMEM -> [BN][128] fp32 tile in the idle pipeline smem (all MMAs, hence all
   // smem reads by the tensor core, are complete once `accum` fires).
   DBG(3);
-  if (push) {
+  if (push || ring) {
     // TMEM -> registers (sum of the 3xTF32 accumulators) -> this CTA's idle ring
     // smem as one contiguous [rows_per cols][128 ch] block per owning rank;
     // one thread bulk-copies each block into its owner's receive slot (TMA
@@ -367,10 +381,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       tc::fence_proxy_async_smem();   // generic-proxy writes -> the bulk copy engine
     }
     tc::tc_fence_before();
-    __syncthreads();
+    // push: the owners' receive buffers sit behind their rings (always free);
+    // ring: they are the owners' rings past the staged blocks, free once every
+    // rank has drained its accumulators, i.e. after one cluster barrier
+    float* rbuf = push ? recv : reinterpret_cast<float*>(smem + stage_bytes);
+    if (ring)
+      tc::cluster_sync();
+    else
+      __syncthreads();
     if (tid == 0) {
       const uint32_t block = static_cast<uint32_t>(128 * rp * 4);
-      const uint32_t rbar_s = tc::smem_u32(rbar), recv_s = tc::smem_u32(recv), stage_s = tc::smem_u32(stage);
+      const uint32_t rbar_s = tc::smem_u32(rbar), recv_s = tc::smem_u32(rbuf), stage_s = tc::smem_u32(stage);
       for (int o = 0; o < a.splits && o * rp < BN; ++o)
         tc::bulk_s2cluster(tc::map_cluster(recv_s + me * block, o), stage_s + o * block, block,
                            tc::map_cluster(rbar_s, o));
@@ -391,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
         for (int z = 0; z < kMaxSplits; ++z)
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (z < a.splits) part[z][e] = recv[(z * rp + c0 + e) * 128 + tid];
+            if (z < a.splits) part[z][e] = rbuf[(z * rp + c0 + e) * 128 + tid];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float acc = part[0][e];

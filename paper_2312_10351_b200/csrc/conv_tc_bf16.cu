@@ -179,20 +179,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   }
 #endif
   // the push epilogue's owner reduction: thread = output channel
-  const float push_bias = (a.push && a.bias && tid < 128 && mt * 128 + tid < a.Cout) ? __ldg(a.bias + mt * 128 + tid) : 0.f;
+  const float push_bias = ((a.push || a.splits > 1) && a.bias && tid < 128 && mt * 128 + tid < a.Cout) ? __ldg(a.bias + mt * 128 + tid) : 0.f;
 
   // push-mode split-K: receive buffer [src rank][128 channels][rows_per columns]
   // fp32 behind the ring (other CTAs may push while this CTA's ring is busy)
   uint64_t* rbar = accum + 2;
   float* recv = reinterpret_cast<float*>(smem + kStages * kStage + bf_bar_bytes(kStages));
   const bool push = a.push != 0;
+  // Opt-in (-DOPARA_RING_PULL) pull-mode split-K without DSMEM loads: after one
+  // cluster barrier every rank bulk-copies its staged blocks into the owners'
+  // (now idle) rings.  Measured slower than the DSMEM pull in graphs
+  // (GoogLeNet fp32 0.234 -> 0.246 ms, BERT 0.482 -> 0.485 ms), so off by default.
+  const uint32_t stage_bytes = static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4);
+#ifndef OPARA_RING_PULL
+  const bool ring = false;
+#else
+  const bool ring = !push && !a.ws && a.splits > 1 && 2 * stage_bytes <= kStages * kStage;
+#endif
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], 32 * kGatherWarps + 1);  // gather threads + the weight loader
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(accum, 1);
-    if (push) tc::mbar_init(rbar, 1);
+    if (push || ring) tc::mbar_init(rbar, 1);
     tc::fence_barrier_init();
   }
   constexpr int kTmemWarp = kMmaWarp;   // the MMA warp is idle in every epilogue: it frees TMEM off the critical path
@@ -208,6 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4));
     }
   } else {
+    if (ring && tid == 0) {   // owners expect every rank's block (the epilogue's cluster barrier orders it)
+      const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
+      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, stage_bytes);
+    }
     __syncthreads();
   }
   tc::tc_fence_after();
@@ -592,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     trace_end(trace);
     return;
   }
-  if (push) {
+  if (push || ring) {
     // TMEM -> registers -> this CTA's smem (the drained ring), laid out as one
     // contiguous [128 channels][rows_per] block per owning rank; then one
     // thread bulk-copies each block into its owner's receive slot (TMA engine,
@@ -621,11 +635,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       if (tid == 0) PHASE(8);
     }
     tc::tc_fence_before();
-    __syncthreads();
+    // push: the owners' receive buffers sit behind their rings (always free);
+    // ring: they are the owners' rings past the staged blocks, free once every
+    // rank has drained its accumulator, i.e. after one cluster barrier
+    float* rbuf = push ? recv : reinterpret_cast<float*>(smem + stage_bytes);
+    if (ring)
+      tc::cluster_sync();
+    else
+      __syncthreads();
     if (tid == 0) {
       PHASE(9);
       const uint32_t block = static_cast<uint32_t>(128 * rp * 4);
-      const uint32_t rbar_s = tc::smem_u32(rbar), recv_s = tc::smem_u32(recv), stage_s = tc::smem_u32(stage);
+      const uint32_t rbar_s = tc::smem_u32(rbar), recv_s = tc::smem_u32(rbuf), stage_s = tc::smem_u32(stage);
       for (int o = 0; o < a.splits && o * rp < BN; ++o)
         tc::bulk_s2cluster(tc::map_cluster(recv_s + me * block, o), stage_s + o * block, block,
                            tc::map_cluster(rbar_s, o));
@@ -651,7 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
           for (int z = 0; z < kMaxSplits; ++z)
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (z < a.splits) part[z][e] = recv[(z * rp + c0 + e) * 128 + chl];
+              if (z < a.splits) part[z][e] = rbuf[(z * rp + c0 + e) * 128 + chl];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             float acc = part[0][e];

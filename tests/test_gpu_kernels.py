@@ -66,7 +66,7 @@ CONV_CASES = [
 ]
 
 
-@pytest.mark.parametrize("engine_name", ["tc", "simt"])
+@pytest.mark.parametrize("engine_name", ["tc", "tc-pull", "simt"])
 @pytest.mark.parametrize("case", CONV_CASES, ids=[str(c) for c in CONV_CASES])
 def test_conv_matches_torch(case, engine_name):
     """Oracle: the same module in float64 on the CPU (cuDNN fp32 may pick
@@ -76,14 +76,15 @@ def test_conv_matches_torch(case, engine_name):
     torch.manual_seed(0)
     m = Wrap(cin, cout, k, s, p, hw).eval()
     x = torch.randn(1, 3, hw, hw)
-    sg = engine.compile(m, x, device=0, profile_reps=2, conv_engine=engine_name)
+    sg = engine.compile(m, x, device=0, profile_reps=2, conv_engine=engine_name.split("-")[0],
+                        splitk="pull" if engine_name.endswith("pull") else None)
     y = sg.run(x.cuda())
     with torch.no_grad():
         ref = m.double()(x.double())
     y_nchw = y.permute(0, 3, 1, 2).cpu()
     assert y_nchw.shape == ref.shape
     # 3xTF32 drops the lo*lo term: ~1e-6 over K ~ 2.6k; exact-fp32 SIMT ~3e-7
-    assert _rel(y_nchw, ref) < (1e-5 if engine_name == "tc" else 2e-6)
+    assert _rel(y_nchw, ref) < (1e-5 if engine_name.startswith("tc") else 2e-6)
     # replaying twice is idempotent (split-K counters reset themselves)
     y2 = sg.run(x.cuda())
     assert torch.equal(y, y2)
@@ -99,16 +100,19 @@ BF16_CASES = [
 ]
 
 
+@pytest.mark.parametrize("splitk", ["push", "pull"])
 @pytest.mark.parametrize("case", BF16_CASES, ids=[str(c) for c in BF16_CASES])
-def test_conv_bf16_matches_torch(case):
+def test_conv_bf16_matches_torch(case, splitk):
     """bf16 tcgen05 engine (kind::f16, fp32 accumulation) vs the fp64 module;
-    bf16 storage of inputs/weights/outputs bounds the error near 1e-2."""
+    bf16 storage of inputs/weights/outputs bounds the error near 1e-2.  Both
+    split-K reductions: push (receive buffers behind the ring) and pull (one
+    cluster barrier, blocks bulk-copied into the owners' rings)."""
     from paper_2312_10351_b200 import engine
     cin, cout, k, s, p, hw = case
     torch.manual_seed(0)
     m = Wrap(cin, cout, k, s, p, hw).eval()
     x = torch.randn(1, 3, hw, hw)
-    sg = engine.compile(m, x, device=0, profile_reps=2, dtype="bf16")
+    sg = engine.compile(m, x, device=0, profile_reps=2, dtype="bf16", splitk=splitk)
     assert all(engine.conv_engine_for(o, 1) == 2 for o in sg.program.ops if o.kind == 1)
     y = sg.run(x.cuda())
     with torch.no_grad():
