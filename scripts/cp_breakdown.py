@@ -28,7 +28,7 @@ while v:
     v = par[v]
 names = {0: "nop", 1: "conv/gemm", 2: "maxpool", 3: "avgpool", 4: "gap", 5: "linear", 6: "add", 7: "layernorm",
          9: "embedding", 10: "attention", 11: "copy", 12: "fm", 13: "dwconv", 14: "relu", 16: "field_emb",
-         17: "first_order"}
+         17: "first_order", 18: "pack_input"}
 cp = collections.defaultdict(lambda: [0, 0.0])
 tot = collections.defaultdict(lambda: [0, 0.0])
 for v in path:
