@@ -97,6 +97,9 @@ __device__ __forceinline__ void load_vec_plain(const T* src, float* f) {
     const float2 t0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
     const float2 t1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
     f[0] = t0.x; f[1] = t0.y; f[2] = t1.x; f[3] = t1.y;
+  } else if constexpr (sizeof(T) == 4 && V == 2) {
+    const float2 r = *reinterpret_cast<const float2*>(src);
+    f[0] = r.x; f[1] = r.y;
   } else {
 #pragma unroll
     for (int e = 0; e < V; ++e) {
@@ -378,16 +381,18 @@ opara_status launch_dwconv2d(const opara_op& op, cudaStream_t s, unsigned long l
     vw = 2;
   const int ks = (a.kh == a.kw && (a.kh == 3 || a.kh == 5 || a.kh == 7)) ? a.kh : 0;
   LaunchCfg c;
-  // tiled shared-memory kernel for 16-byte vectors (bf16: 8-byte ones when the
+  // tiled shared-memory kernel for 16-byte vectors (8-byte ones when the
   // 16-byte tiling would leave fewer than two CTAs per SM), square windows,
   // equal strides 1/2
-  const bool tiled_ok = bf ? vw >= 4 : vw == V;
+  const bool tiled_ok = vw >= V / 2;
   if (tiled_ok && ks && a.sh == a.sw && (a.sh == 1 || a.sh == 2) && !tiled_disabled()) {
     size_t smem = 0;
     const int64_t tiles = static_cast<int64_t>((a.OW + kTile - 1) / kTile) * ((a.OH + kTile - 1) / kTile) * a.N;
-    const int tv = !bf ? V : (vw == 8 && tiles * ((a.C + kCV * 8 - 1) / (kCV * 8)) >= 2 * 148) ? 8 : 4;
-    c.func = !bf ? pick_tiled<float, 4>(ks, a.sh, &smem)
-                 : tv == 8 ? pick_tiled<__nv_bfloat16, 8>(ks, a.sh, &smem) : pick_tiled<__nv_bfloat16, 4>(ks, a.sh, &smem);
+    const int tv = (vw == V && tiles * ((a.C + kCV * V - 1) / (kCV * V)) >= 2 * 148) ? V : V / 2;
+    if (bf)
+      c.func = tv == 8 ? pick_tiled<__nv_bfloat16, 8>(ks, a.sh, &smem) : pick_tiled<__nv_bfloat16, 4>(ks, a.sh, &smem);
+    else
+      c.func = tv == 4 ? pick_tiled<float, 4>(ks, a.sh, &smem) : pick_tiled<float, 2>(ks, a.sh, &smem);
     if (c.func) {
       const int cgroups = (a.C + kCV * tv - 1) / (kCV * tv);
       c.block = dim3(kTile * kTile * kCV);
