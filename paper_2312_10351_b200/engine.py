@@ -140,15 +140,29 @@ def pack_conv_weights_tf32x3(wk: np.ndarray, rows: int = 128) -> np.ndarray:
     return np.ascontiguousarray(np.stack([image(hi), image(lo)], axis=2)).reshape(-1)
 
 
-def dag_levels(program: Program) -> list[int]:
-    """Longest-path depth of every op (ops are emitted in topological order)."""
-    preds = [[] for _ in program.ops]
+def dag_levels(program: Program, alap: bool | None = None) -> list[int]:
+    """Longest-path depth of every op (ops are emitted in topological order).
+    alap=True: as-late-as-possible levels instead (depth minus the longest
+    path to a sink), which puts a short branch beside the tail of the long
+    branches it actually runs next to; OPARA_LEVELS=alap selects it."""
+    if alap is None:
+        alap = os.environ.get("OPARA_LEVELS", "") == "alap"
+    n = len(program.ops)
+    preds = [[] for _ in range(n)]
+    succs = [[] for _ in range(n)]
     for u, v in program.edges:
         preds[v].append(u)
-    level = [0] * len(program.ops)
-    for v in range(len(program.ops)):
+        succs[u].append(v)
+    level = [0] * n
+    for v in range(n):
         level[v] = 1 + max((level[u] for u in preds[v]), default=-1)
-    return level
+    if not alap:
+        return level
+    tail = [0] * n                      # longest path (in ops) from v to a sink
+    for v in range(n - 1, -1, -1):
+        tail[v] = 1 + max((tail[w] for w in succs[v]), default=-1)
+    depth = max(level[v] + tail[v] for v in range(n)) if n else 0
+    return [depth - tail[v] for v in range(n)]
 
 
 def concurrent_convs(program: Program) -> dict[int, int]:
