@@ -204,15 +204,38 @@ def concurrency_targets(program: Program, num_sms: int = 148, scale: float = 1.0
     full-GPU grid: there is nothing to co-reside with."""
     level = dag_levels(program)
     serial = serial_ops(program)
-    work: dict[int, int] = {}
+    weight = _path_weights(program) if os.environ.get("OPARA_SHARES", "") == "slack" else None
+    w = (lambda v: program.ops[v].flops * weight[v]) if weight else (lambda v: program.ops[v].flops)
+    work: dict[int, float] = {}
     for v, op in enumerate(program.ops):
         if op.kind == CONV2D:
-            work[level[v]] = work.get(level[v], 0) + op.flops
+            work[level[v]] = work.get(level[v], 0) + w(v)
     out = {}
     for v, op in enumerate(program.ops):
         if op.kind == CONV2D and work.get(level[v]) and v not in serial:
-            out[v] = max(8, int(round(scale * num_sms * op.flops / work[level[v]])))
+            out[v] = max(8, int(round(scale * num_sms * w(v) / work[level[v]])))
     return out
+
+
+def _path_weights(program: Program) -> list[float]:
+    """(longest estimated-latency path through op v / critical path)^2: ops
+    with slack get smaller SM shares than the critical chain beside them
+    (OPARA_SHARES=slack).  Latency model: 2 us + FLOPs at 50 TFLOP/s."""
+    n = len(program.ops)
+    cost = [2.0 + (op.flops / 50e6 if op.kind == CONV2D else 0.0) for op in program.ops]
+    preds = [[] for _ in range(n)]
+    succs = [[] for _ in range(n)]
+    for u, v in program.edges:
+        preds[v].append(u)
+        succs[u].append(v)
+    head = [0.0] * n
+    for v in range(n):
+        head[v] = cost[v] + max((head[u] for u in preds[v]), default=0.0)
+    tail = [0.0] * n
+    for v in range(n - 1, -1, -1):
+        tail[v] = cost[v] + max((tail[x] for x in succs[v]), default=0.0)
+    cp = max(head) if n else 1.0
+    return [((head[v] + tail[v] - cost[v]) / cp) ** 2 for v in range(n)]
 
 
 SPLITK_MODES = {"push": 0, "pull": 1, "global": 2}
