@@ -662,7 +662,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     if (mine > 0 && tid < 128) {
       tc::mbar_wait_cluster(rbar, 0);
       if (tid == 0) PHASE(5);
-      if (tid == 0) PHASE(6);
       TO* out = static_cast<TO*>(a.out);
       const int chl = tid, ch = mt * 128 + chl;
       if (ch < a.Cout) {
@@ -690,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
         }
       }
     }
+    if (tid == 0) PHASE(6);   // owner reduction done; exit waits for this CTA's outgoing copies
     if (tid == 0) tc::bulk_wait_read();   // the source blocks stay valid until the engine has read them
     PHASE_FLUSH();
     trace_end(trace);
