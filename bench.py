@@ -1,20 +1,30 @@
 """Benchmark: batch-1 inference through the Opara multi-stream CUDA Graph.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--model inception_v3|googlenet]
-    python bench.py --impl reference ...     # the reference's CPU path (oracle port)
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--model inception_v3|googlenet|...]
+    python bench.py --impl reference ...     # the reference's CPU path on the same DAG
 
-A "step" is one batch-1 inference = one replay of the captured graph.  Every
-rank (one per GPU, torchrun for N > 1) owns an independent replica — the path
-does not shard, there is no collective on the data path; the
-only cross-rank traffic is the max-over-ranks timing reduction.
+A "step" is one inference of `--batch` requests = one replay of the captured
+graph.  Every rank (one per GPU, torchrun for N > 1) owns an independent
+replica — the path does not shard and there is no collective
+on the data path.  The only cross-rank traffic is control: a gloo (CPU)
+process group broadcasts rank 0's tuning choice and reduces the timed
+seconds with a max — no NCCL.
 
 The JSON line carries: value (whole-job inferences/s, device-timed, L2
 flushed before every step), latency and the speed-up over the sequential
-single-stream CUDA Graph of the same kernels, the DAG roofline fraction, the
-dominant kernel's roofline, e2e (pinned host input -> H2D -> replay -> D2H of
-the logits, through ScheduledGraph.run_host), clocks sampled during the timed
-region, and cpu_baseline (the reference's CPU path: oracle port of
-allocate_streams + order_opara + simulate on the same profiled DAG).
+single-stream CUDA Graph of the same kernels, the DAG and hardware roofline
+fractions, the dominant kernel's roofline, e2e (pinned host input -> H2D ->
+replay -> D2H of the output, through ScheduledGraph.run_host), clocks sampled
+during the timed region, the schedule files of the timed graph, and
+cpu_baseline (the reference's CPU path — its own ``opsched`` package from
+baseline/_ref, else the oracle port — on the same profiled DAG).  The run
+fails (exit 1) when the timed graph's output misses the north_star tolerance
+or its schedule differs from the reference's.
+
+``--impl reference`` never imports this repo's package: it loads the
+profiled DAG committed under schedules/<workload>/ (written by an earlier GPU
+run of this bench) and runs load_graph + allocate_streams + order_opara +
+simulate through the reference package on every host core.
 """
 
 from __future__ import annotations
@@ -29,8 +39,13 @@ import threading
 import time
 from pathlib import Path
 
+# read once by the CUDA driver at context creation: one hardware queue per plan stream
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+SCHEDULES = ROOT / "schedules"      # committed profiled DAGs + schedules, one dir per workload
+REF_PKG = ROOT / "baseline" / "_ref"  # pip --target install of the reference (stdlib-only)
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FP32_SIMT_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 TF/s FFMA, nominal
@@ -112,38 +127,109 @@ def _dist():
 # ------------------------------------------------------------ CPU baseline
 
 
+def _reference_api():
+    """"reference" when the reference's own ``opsched`` (pip-installed into
+    baseline/_ref, stdlib-only) imports, else "port" (the oracle restatement)."""
+    if REF_PKG.is_dir() and str(REF_PKG) not in sys.path:
+        sys.path.insert(0, str(REF_PKG))
+    try:
+        import opsched  # noqa: F401
+        return "reference"
+    except ImportError:
+        return "port"
+
+
 def _cpu_sim_worker(args):
-    """One process: oracle allocate_streams + order_opara + simulate, repeated
-    until `budget_s` elapses.  Returns (runs, seconds)."""
-    graph_dict, cfg, budget_s = args
+    """One process: the reference's 'scheduled graph out, run' on the DAG file —
+    load_graph + allocate_streams + order_opara + simulate — repeated until
+    `budget_s` elapses.  Returns (runs, seconds, kind)."""
+    graph_path, cfg_path, budget_s = args
     sys.path.insert(0, str(ROOT))
-    from oracle import opsched_oracle as orc
+    kind = _reference_api()
     runs = 0
     t0 = time.perf_counter()
+    if kind == "reference":
+        import opsched
+        cfg = opsched.load_gpu_config(cfg_path)
+        while True:
+            g = opsched.load_graph(graph_path)
+            plan = opsched.allocate_streams(g)
+            sched = opsched.order_opara(g, cfg)
+            opsched.simulate(g, plan, sched, cfg)
+            runs += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s:
+                return runs, el, kind
+    from oracle import opsched_oracle as orc
+    cfg = json.loads(Path(cfg_path).read_text())
     while True:
-        g = orc.Dag(graph_dict["nodes"], graph_dict["edges"])
+        d = json.loads(Path(graph_path).read_text())
+        g = orc.Dag(d["nodes"], d["edges"])
         a, ns, sync = orc.allocate_streams(g)
         order = orc.order_opara(g, cfg)
         orc.simulate_makespan_ns(g, a, ns, sync, order, cfg)
         runs += 1
         el = time.perf_counter() - t0
         if el >= budget_s:
-            return runs, el
+            return runs, el, kind
 
 
-def cpu_reference(graph_dict: dict, cfg: dict, budget_s: float, procs: int) -> dict:
+def cpu_reference(graph_path, cfg_path, budget_s: float, procs: int) -> dict:
     """The reference's CPU path on this host: `procs` processes in parallel."""
     if procs <= 1:
-        runs, el = _cpu_sim_worker((graph_dict, cfg, budget_s))
+        runs, el, kind = _cpu_sim_worker((str(graph_path), str(cfg_path), budget_s))
         total = runs / el
     else:
         import multiprocessing as mp
         ctx = mp.get_context("spawn")
         with ctx.Pool(procs) as pool:
-            res = pool.map(_cpu_sim_worker, [(graph_dict, cfg, budget_s)] * procs)
-        total = sum(r / e for r, e in res)
-        runs = sum(r for r, _ in res)
-    return {"value": total, "runs": runs}
+            res = pool.map(_cpu_sim_worker, [(str(graph_path), str(cfg_path), budget_s)] * procs)
+        total = sum(r / e for r, e, _ in res)
+        runs = sum(r for r, _, _ in res)
+        kind = res[0][2]
+    return {"value": total, "runs": runs, "kind": kind}
+
+
+def reference_schedule(graph_path, cfg_path) -> dict:
+    """The checker: the reference's (or the oracle's) Alg. 1 plan and Alg. 2
+    order of the DAG file, as plain data."""
+    kind = _reference_api()
+    if kind == "reference":
+        import opsched
+        g = opsched.load_graph(graph_path)
+        plan = opsched.allocate_streams(g)
+        order = opsched.order_opara(g, opsched.load_gpu_config(cfg_path)).order
+        return {"assignment": dict(plan.assignment), "num_streams": plan.num_streams,
+                "sync": [tuple(e) for e in plan.sync_events], "order": list(order), "kind": kind}
+    from oracle import opsched_oracle as orc
+    d = json.loads(Path(graph_path).read_text())
+    g = orc.Dag(d["nodes"], d["edges"])
+    a, ns, sync = orc.allocate_streams(g)
+    return {"assignment": a, "num_streams": ns, "sync": [tuple(e) for e in sync],
+            "order": orc.order_opara(g, json.loads(Path(cfg_path).read_text())), "kind": kind}
+
+
+def cpu_model_execution(model, x, budget_s: float) -> dict:
+    """BASELINE.md §3's CPU model-execution analog: PyTorch eager fp32 forward on
+    every host core, repeated for `budget_s`."""
+    import torch
+    cores = len(os.sched_getaffinity(0))
+    prev = torch.get_num_threads()
+    torch.set_num_threads(cores)
+    model = model.cpu().eval()
+    xs = tuple(t.cpu() for t in x) if isinstance(x, tuple) else (x.cpu(),)
+    runs = 0
+    with torch.no_grad():
+        model(*xs)
+        t0 = time.perf_counter()
+        while True:
+            model(*xs)
+            runs += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s:
+                break
+    torch.set_num_threads(prev)
+    return {"runs": runs, "seconds": el, "cores": cores}
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -154,19 +240,36 @@ def build_workload(args):
     from paper_2312_10351_b200 import zoo
     if args.model == "bert_base":
         model, ref_model, x = zoo.build_bert()
-        args.dtype = "bf16"  # BASELINE config: BERT-base seq 128 bf16
         return model, ref_model, x
     if args.model == "deepfm":
         model, x = zoo.build_deepfm(args.batch)
-        args.dtype = "f32"   # fp32 recommendation model (the MLP runs on the exact-fp32 engine)
         return model, model, x
     model, x = zoo.build(args.model, batch=args.batch)
     return model, model, x
 
 
+def resolve_dtype(args) -> None:
+    if args.model == "bert_base":
+        args.dtype = "bf16"  # BASELINE config: BERT-base seq 128 bf16
+    elif args.model == "deepfm":
+        args.dtype = "f32"   # fp32 recommendation model (exact-fp32 engines)
+
+
+def workload_key(args) -> str:
+    return f"{args.model}_{args.dtype}_b{args.batch}"
+
+
 def workload_name(args, x) -> str:
     shape = "+".join("x".join(map(str, t.shape)) for t in (x if isinstance(x, tuple) else (x,)))
     return f"{args.model} batch={args.batch} {args.dtype} ({shape})"
+
+
+def bench_config(meta: dict, world: int) -> dict:
+    """The `config` object both arms print (same workload, same DAG)."""
+    return {"workload": meta["workload"], "parallelism": f"{world} independent replica(s), no collective",
+            "l2": "flushed (256 MiB memset) before every timed step, outside the event bracket",
+            "dag_nodes": meta["dag_nodes"], "dag_edges": meta["dag_edges"],
+            "streams": meta["streams"], "syncs": meta["syncs"], "schedule": meta["schedule"]}
 
 
 def broadcast_value(dist, rank: int, compute):
@@ -176,50 +279,117 @@ def broadcast_value(dist, rank: int, compute):
     return box[0]
 
 
-def run_gpu(args) -> dict | None:
+def replica_compile(dist, rank: int, world: int, search, build_choice, cache_dir):
+    """Replicas run identical graphs.  Rank 0 runs `search(cache_path)` (the
+    sizing-variant search, which writes its tile choices into the tuning cache
+    file), then broadcasts its variant and the cache CONTENTS; every other rank
+    writes them into its own local cache file and calls
+    `build_choice(variant, cache_path)`.  Control traffic only, over the
+    (gloo) process group.  Returns (scheduled graph, variant)."""
+    cache = os.path.join(cache_dir, f"opara_tune_rank{rank}.json")
+    sg = search(cache) if rank == 0 else None
+    variant, text = broadcast_value(dist, rank, lambda: (sg_variant(sg), Path(cache).read_text()
+                                                         if os.path.exists(cache) else "{}"))
+    if rank != 0:
+        Path(cache).write_text(text)
+        sg = build_choice(variant, cache)
+    return sg, variant
+
+
+def sg_variant(sg) -> tuple:
+    return (bool(sg.bound_grids), sg.splitk, sg.bound_scale)
+
+
+def time_max(dist, world: int, values: list[float]) -> list[float]:
+    """Max over ranks of per-rank device-timed seconds (gloo, CPU tensors)."""
+    if world <= 1:
+        return values
+    import torch
+    t = torch.tensor(values, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def measure_tf32_tflops(dev) -> float:
+    """Dense TF32 tensor throughput of this GPU (cuBLAS 8192^3 GEMM, TF32 on):
+    the measured denominator of the 3xTF32 engine's roofline (÷3 passes)."""
+    import torch
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    n = 8192
+    a = torch.randn(n, n, device=dev)
+    b = torch.randn(n, n, device=dev)
+    for _ in range(3):
+        a @ b
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    it = 20
+    e0.record()
+    for _ in range(it):
+        a @ b
+    e1.record()
+    torch.cuda.synchronize()
+    torch.backends.cuda.matmul.allow_tf32 = old
+    ms = e0.elapsed_time(e1) / it
+    del a, b
+    return 2 * n ** 3 / (ms * 1e-3) / 1e12
+
+
+def save_schedule(sg, args, meta: dict, root: Path) -> Path:
+    """The timed graph's profiled DAG, plan, order and GpuConfig (reference file
+    formats) plus the workload meta, so the numbers tie to a re-checkable schedule."""
+    from paper_2312_10351_b200.device import gpu_config_to_dict
+    d = root / workload_key(args)
+    sg.save(d)
+    (d / "gpu_config.json").write_text(json.dumps(gpu_config_to_dict(sg.gpu_config), indent=2, sort_keys=True) + "\n")
+    (d / "meta.json").write_text(json.dumps(meta, indent=2, sort_keys=True) + "\n")
+    return d
+
+
+def run_gpu(args) -> tuple[dict | None, int]:
     import torch
     import torch.distributed as dist
 
     world, rank, local = _dist()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # control plane only (tuning choice broadcast, max-over-ranks timing): gloo on the host
+        dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     torch.backends.cudnn.allow_tf32 = False
     torch.backends.cuda.matmul.allow_tf32 = False
 
-    from paper_2312_10351_b200 import engine, zoo
-    from paper_2312_10351_b200.dag import graph_to_dict
+    from paper_2312_10351_b200 import engine
 
     model, ref_model, x = build_workload(args)
     bound = {"auto": "auto", "bounded": True, "full": False}[args.grids]
-    if world > 1 and bound == "auto":
-        # replicas run identical graphs: rank 0 searches the sizing variants and
-        # tiles once, the other ranks compile its choice from the shared tuning cache
+
+    def compile_auto(cache_path=None):
+        if cache_path:
+            os.environ["OPARA_TUNE_CACHE"] = cache_path
+        return engine.compile(model, x, device=local, bound_grids=bound, profile_reps=args.profile_reps,
+                              dtype=args.dtype)
+
+    def compile_choice(variant, cache_path):
+        os.environ["OPARA_TUNE_CACHE"] = cache_path
+        bounded, splitk, scale = variant
+        return engine.ScheduledGraph(engine.lower(model, x, args.dtype), local, profile_reps=args.profile_reps,
+                                     bound_grids=bounded, splitk=splitk, bound_scale=scale)
+
+    if world > 1:
         import tempfile
-        os.environ["OPARA_TUNE_CACHE"] = broadcast_value(dist, rank, lambda: os.environ.get("OPARA_TUNE_CACHE") or
-                                                         os.path.join(tempfile.gettempdir(),
-                                                                      f"opara_tune_{os.getpid()}.json"))
-        sg = None
-        if rank == 0:
-            sg = engine.compile(model, x, device=local, bound_grids="auto", profile_reps=args.profile_reps,
-                                dtype=args.dtype)
-        bounded, splitk, scale = broadcast_value(dist, rank, lambda: (sg.bound_grids, sg.splitk, sg.bound_scale))
-        if rank != 0:
-            program = engine.lower(model, x, args.dtype)
-            sg = engine.ScheduledGraph(program, local, profile_reps=args.profile_reps, bound_grids=bounded,
-                                       splitk=splitk, bound_scale=scale)
+        sg, _ = replica_compile(dist, rank, world, compile_auto, compile_choice, tempfile.gettempdir())
     else:
-        sg = engine.compile(model, x, device=local, bound_grids=bound, profile_reps=args.profile_reps,
-                            dtype=args.dtype)
+        sg = compile_auto()
     xd = tuple(t.cuda(local) for t in x) if isinstance(x, tuple) else x.cuda(local)
-    # correctness guard on every rank: a fast wrong answer is not a result
+    # correctness gate on every rank, on the graph that is timed: a fast wrong answer is not a result
     y = sg.run(xd)
     y = y[0] if isinstance(y, tuple) else y
     with torch.no_grad():
         ref = ref_model.cuda(local)(*xd) if isinstance(xd, tuple) else ref_model.cuda(local)(xd)
     ref = ref[0] if isinstance(ref, tuple) else ref
     y = y.float().reshape(ref.shape)
-    rel = (torch.linalg.vector_norm(y - ref) / torch.linalg.vector_norm(ref)).item()
+    rel = (torch.linalg.vector_norm(y.double() - ref.double()) / torch.linalg.vector_norm(ref.double())).item()
+    tol = 1e-4 if args.dtype == "f32" else 1e-2
     ref_model.cpu()
     del ref
     torch.cuda.synchronize()
@@ -260,30 +430,23 @@ def run_gpu(args) -> dict | None:
         sg.capture(slot, sg.plan, make_order(sg.graph, pol, sg.gpu_config))
         orders[pol] = round(sg.time(slot, warmup=args.warmup, iters=args.steps, flush_l2=True).median_ms, 4)
 
-    # e2e through the public API: pinned host in -> H2D -> replay -> D2H logits
+    # e2e through the public API: pinned host in -> H2D -> replay -> D2H output
     e2e = sg.time_host_roundtrip(x, warmup=args.warmup, iters=args.steps)
 
-    if world > 1:
-        tt = torch.tensor([step_total_s, e2e["seconds"]], dtype=torch.float64, device=torch.device("cuda", local))
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        step_total_s, e2e_s = tt.tolist()
-    else:
-        e2e_s = e2e["seconds"]
-
+    step_total_s, e2e_s = time_max(dist, world, [step_total_s, e2e["seconds"]])
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
-        return None
+        return None, 0 if rel <= tol else 1
 
     peaks = _peaks()
+    tf32_tflops = measure_tf32_tflops(sg.dev)
     work = sg.work()
     cp_us = sg.critical_path_us()
     lat_ms = t_par.median_ms
-    # Compute peaks per engine.  tcgen05 kind::tf32 runs at half the bf16 rate
-    # (tensor throughput scales with operand bytes), and 3xTF32 issues three
-    # MMAs per product: effective peak = measured bf16 / 2 / 3.  The SIMT
-    # engine's peak is the nominal fp32 FFMA rate (no measured figure exists).
-    tc_peak_tflops = peaks["bf16_tflops"] / 2 / 3
+    # compute peaks per engine: 3xTF32 = measured TF32 / 3 passes; bf16 = measured
+    # (MEASURED_PEAKS.json); the SIMT engine's peak is the nominal fp32 FFMA rate
+    tc_peak_tflops = tf32_tflops / 3
     fam = {}
     for k, (op, p) in enumerate(zip(sg.program.ops, sg.profile)):
         if op.kind == 0:
@@ -313,49 +476,46 @@ def run_gpu(args) -> dict | None:
     total_us = sum(f["us"] for f in fam.values())
     if dom in peak_of:
         achieved = d["flops"] / (d["us"] * 1e-6) / 1e12
-        peak, unit, bound = peak_of[dom], "TFLOP/s", "tensor"
+        peak, unit, bound_kind = peak_of[dom], "TFLOP/s", "tensor"
     else:
         achieved = d["bytes"] / (d["us"] * 1e-6) / 1e9
-        peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
-    traffic = None
-    prof = ROOT / "profiles" / f"r01_{args.model}_{args.dtype}_full.md"
-    if prof.exists() and dom in prof.read_text():
-        vals = {}
-        for ln in prof.read_text().splitlines():
-            parts = [x.strip() for x in ln.split("|")]
-            if len(parts) > 3 and parts[1].startswith("dram__bytes_"):
-                mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(parts[2], 1)
-                vals[parts[1]] = float(parts[3]) * mult
-        if vals:
-            traffic = int(sum(vals.values()))
+        peak, unit, bound_kind = peaks["hbm_gbs"], "GB/s", "hbm"
+    traffic, traffic_note = _ncu_traffic(args, dom)
     roofline = {
         "kernel": dom,
-        "bound": bound,
+        "bound": bound_kind,
         "achieved": round(achieved, 3), "peak": round(peak, 1),
         "unit": unit, "frac": round(achieved / peak, 4),
-        "peak_source": ("measured bf16 (MEASURED_PEAKS.json) / 2 (tf32 rate) / 3 (3xTF32 passes)"
+        "peak_source": ("measured TF32 (cuBLAS 8192^3 GEMM, TF32 on, this run) / 3 (3xTF32 passes)"
                         if dom == "conv2d_tc_tf32x3" else
                         "measured bf16 dense (MEASURED_PEAKS.json)" if dom in ("conv2d_tc_bf16", "attention_tc") else
                         "nominal fp32 FFMA (148 SM x 128 lanes x 2 x 1.965 GHz)" if unit == "TFLOP/s"
                         else "measured HBM copy (MEASURED_PEAKS.json)"),
         "traffic": traffic,
-        "traffic_note": f"dram read+write bytes of one {dom} launch from the committed ncu --set full capture "
-                        f"({prof.name}, cold cache under ncu)" if traffic else None,
+        "traffic_note": traffic_note,
         "share_of_step": round(d["us"] / total_us, 3),
         "launches_per_step": d["launches"],
         "flops_per_step": d["flops"],
+        "bytes_per_step": d["bytes"],
+        "avg_launch_us": round(d["us"] / d["launches"], 3),
         "timing": "CUDA events around a graph of back-to-back launches of each op (opara_exec_profile), "
                   "summed over the family's launches",
     }
 
-    # CPU baseline: the reference's path on the same profiled DAG, 1 core
-    gd = graph_to_dict(sg.graph)
-    gcfg = {"num_sms": sg.gpu_config.num_sms, "threads_per_sm": sg.gpu_config.threads_per_sm,
-            "shared_mem_per_sm": sg.gpu_config.shared_mem_per_sm,
-            "registers_per_sm": sg.gpu_config.registers_per_sm,
-            "max_blocks_per_sm": sg.gpu_config.max_blocks_per_sm,
-            "same_class_slowdown": sg.gpu_config.same_class_slowdown}
-    cpu = cpu_reference(gd, gcfg, args.cpu_seconds, 1)
+    # the timed graph's schedule, saved in the reference's file formats and
+    # re-checked against the reference's own Alg. 1 / Alg. 2 on the same DAG file
+    meta = {"workload": workload_name(args, x), "dag_nodes": len(sg.graph), "dag_edges": len(sg.graph.edges),
+            "streams": sg.plan.num_streams, "syncs": len(sg.plan.sync_events),
+            "schedule": f"schedules/{workload_key(args)}"}
+    out_root = Path(args.save_schedule) if args.save_schedule else ROOT / "gpurun_out" / "schedules"
+    sdir = save_schedule(sg, args, meta, out_root)
+    chk = reference_schedule(sdir / "graph.json", sdir / "gpu_config.json")
+    sched_ok = (chk["assignment"] == dict(sg.plan.assignment) and chk["num_streams"] == sg.plan.num_streams
+                and chk["sync"] == [tuple(e) for e in sg.plan.sync_events]
+                and chk["order"] == list(sg.schedule.order))
+
+    cpu = cpu_reference(sdir / "graph.json", sdir / "gpu_config.json", args.cpu_seconds, 1)
+    cpu_exec = cpu_model_execution(ref_model, x, args.cpu_model_seconds) if args.cpu_model_seconds > 0 else None
 
     launches = sg.num_launches(engine.SLOT_PARALLEL)
     value = world * args.batch * args.steps / step_total_s
@@ -373,11 +533,7 @@ def run_gpu(args) -> dict | None:
         "vs_baseline": None,
         "dtype": args.dtype,
         "data": "synthetic input, random-init weights (seed 0), BN stats randomised",
-        "config": {"workload": workload_name(args, x),
-                   "parallelism": f"{world} independent replica(s), no collective",
-                   "l2": "flushed (256 MiB memset) before every timed step, outside the event bracket",
-                   "dag_nodes": len(sg.graph), "dag_edges": len(sg.graph.edges),
-                   "streams": sg.plan.num_streams, "syncs": len(sg.plan.sync_events)},
+        "config": bench_config(meta, world),
         "latency_ms": round(lat_ms, 4),
         "latency_ms_mean": round(t_par.mean_ms, 4),
         "sequential_latency_ms": round(t_seq.median_ms, 4),
@@ -400,12 +556,21 @@ def run_gpu(args) -> dict | None:
         "dag_roofline": {"critical_path_us": round(cp_us, 2), "flop_term_us": round(flop_term_us, 2),
                          "byte_term_us": round(byte_term_us, 2), "roofline_us": round(roof_us, 2),
                          "frac": round(roof_us / (lat_ms * 1e3), 4),
+                         "hw_frac": round((flop_term_us + byte_term_us) / (lat_ms * 1e3), 4),
+                         "note": "frac = north_star DAG roofline (critical path of this build's own isolated "
+                                 "kernel times); hw_frac = hardware term only (FLOPs at peak + bytes at HBM)",
                          "flops": work["flops"], "bytes": work["bytes"],
                          "compute_peak_tflops": {k: round(v, 1) for k, v in peak_of.items()},
+                         "tf32_tflops_measured": round(tf32_tflops, 1),
                          "hbm_peak_gbs": peaks["hbm_gbs"]},
         "roofline": roofline,
         "rel_err_vs_torch_fp32": rel,
-        "rel_tolerance": 1e-4 if args.dtype == "f32" else 1e-2,
+        "rel_tolerance": tol,
+        "parity_ok": rel <= tol,
+        "schedule_parity": {"ok": sched_ok, "checker": chk["kind"],
+                            "files": [f"{meta['schedule']}/{n}" for n in
+                                      ("graph.json", "plan.json", "order.json", "gpu_config.json")],
+                            "written_to": str(sdir.relative_to(ROOT)) if sdir.is_relative_to(ROOT) else str(sdir)},
         "e2e": {"value": round(world * args.batch * args.steps / e2e_s, 2), "unit": "inferences/s",
                 "h2d_bytes_per_step": e2e["h2d_bytes"], "d2h_bytes_per_step": e2e["d2h_bytes"],
                 "path": "ScheduledGraph.run_host: pinned host input(s) -> H2D -> graph replay -> "
@@ -414,44 +579,75 @@ def run_gpu(args) -> dict | None:
         "gpu_launches_per_step": launches,
         "clocks": clk.summary(),
         "cpu_baseline": {"value": round(cpu["value"] * args.batch, 3), "unit": "inferences/s", "cores": 1,
-                         "kind": "port",
-                         "sample": f"{cpu['runs']} runs of oracle allocate_streams + order_opara + "
-                                   f"simulate (the reference's 'run') on the profiled {args.model} DAG, "
-                                   f"{args.cpu_seconds:.0f} s budget, 1 process"},
+                         "kind": cpu["kind"],
+                         "sample": f"{cpu['runs']} runs of load_graph + allocate_streams + order_opara + "
+                                   f"simulate (the reference's 'scheduled graph out, run') on this run's "
+                                   f"profiled {args.model} DAG file, {args.cpu_seconds:.0f} s budget, 1 process"},
+        "cpu_model_execution": None if cpu_exec is None else {
+            "value": round(cpu_exec["runs"] * args.batch / cpu_exec["seconds"], 3), "unit": "inferences/s",
+            "cores": cpu_exec["cores"],
+            "sample": f"PyTorch eager fp32 forward of the same model on the host, torch.set_num_threads("
+                      f"{cpu_exec['cores']}), {cpu_exec['runs']} runs in {cpu_exec['seconds']:.1f} s"},
         "peaks": peaks,
+        "version": _version(),
     }
     if world > 1:
         dist.destroy_process_group()
-    return line
+    return line, 0 if (rel <= tol and sched_ok) else 1
+
+
+def _version() -> str:
+    from paper_2312_10351_b200 import _lib
+    return _lib.version()
+
+
+def _ncu_traffic(args, dom: str):
+    """DRAM bytes of one launch of the dominant kernel from the committed
+    `ncu --set full` summary of this workload (newest round first)."""
+    for rnd in ("r02", "r01"):
+        prof = ROOT / "profiles" / f"{rnd}_{args.model}_{args.dtype}_full.md"
+        if not prof.exists() or dom not in prof.read_text():
+            continue
+        vals, shape = {}, None
+        for ln in prof.read_text().splitlines():
+            parts = [x.strip() for x in ln.split("|")]
+            if len(parts) > 3 and parts[1].startswith("dram__bytes_"):
+                mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(parts[2], 1)
+                vals[parts[1]] = float(parts[3]) * mult
+            if len(parts) > 3 and parts[1] == "conv shape":
+                shape = parts[3]
+        if vals:
+            note = (f"dram read+write bytes of one {dom} launch from the committed ncu --set full capture "
+                    f"({prof.name}, cold cache under ncu)" + (f"; launch shape {shape}" if shape else ""))
+            return int(sum(vals.values())), note
+    return None, None
 
 
 def run_reference(args) -> dict | None:
-    """--impl reference: the reference's CPU path on all host cores."""
+    """--impl reference: the reference's CPU path on all host cores, on the
+    profiled DAG the GPU arm scheduled (committed under schedules/).  Imports
+    nothing from this repo's package."""
     world, rank, _ = _dist()
     if rank != 0:
         return None
-    from paper_2312_10351_b200 import frontend
-    from paper_2312_10351_b200.dag import graph_to_dict
-    import paper_2312_10351_b200.engine as engine
-    model, _, x = build_workload(args)
-    prog = frontend.lower(model, x, args.dtype)
-    g = engine.static_dag(prog)  # same topology / classes; launch-config demands
-    gd = graph_to_dict(g)
-    cfg = {"num_sms": 148, "threads_per_sm": 2048, "shared_mem_per_sm": 233472,
-           "registers_per_sm": 65536, "max_blocks_per_sm": 32, "same_class_slowdown": 1.4}
+    sdir = SCHEDULES / workload_key(args)
+    if not (sdir / "graph.json").exists():
+        return {"impl": "reference", "unavailable": f"no committed profiled DAG at {sdir.relative_to(ROOT)}"}
+    meta = json.loads((sdir / "meta.json").read_text())
+    graph, cfgp = sdir / "graph.json", sdir / "gpu_config.json"
     cores = len(os.sched_getaffinity(0))
     per_step = max(1.0, args.cpu_seconds / max(1, args.steps))
-    vals = []
     for _ in range(args.warmup):
-        cpu_reference(gd, cfg, 0.2, 1)
+        cpu_reference(graph, cfgp, 0.2, 1)
+    vals, runs, kind = [], 0, None
     t0 = time.perf_counter()
-    runs = 0
     for _ in range(args.steps):
-        r = cpu_reference(gd, cfg, per_step, cores)
+        r = cpu_reference(graph, cfgp, per_step, cores)
         vals.append(r["value"])
         runs += r["runs"]
+        kind = r["kind"]
     el = time.perf_counter() - t0
-    v = statistics.median(vals) * args.batch   # one simulated DAG run serves `batch` requests
+    v = statistics.median(vals) * args.batch   # one scheduled + simulated DAG run serves `batch` requests
     return {
         "impl": "reference",
         "metric": "batch-1 inference throughput (inferences/s); batch-1 latency ms and speed-up vs the "
@@ -459,11 +655,14 @@ def run_reference(args) -> dict | None:
         "value": round(v, 3), "unit": "inferences/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 / v, 3) if v else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic DAG of the model (launch-config demands)",
-        "config": {"workload": workload_name(args, x), "path": "reference CPU path (allocate_streams + "
-                               "order_opara + simulate) on the model's DAG", "processes": cores},
-        "cpu_baseline": {"value": round(v, 3), "unit": "inferences/s", "cores": cores, "kind": "port",
-                         "sample": f"{runs} simulated runs in {el:.1f} s across {cores} processes"},
+        "data": "the GPU arm's profiled DAG of the synthetic model (committed schedule files)",
+        "config": bench_config(meta, world),
+        "path": ("the reference package itself (baseline/_ref/opsched): load_graph + allocate_streams + "
+                 "order_opara + simulate" if kind == "reference" else
+                 "oracle port of load_graph + allocate_streams + order_opara + simulate"),
+        "cpu_baseline": {"value": round(v, 3), "unit": "inferences/s", "cores": cores, "kind": kind,
+                         "sample": f"{runs} scheduled+simulated runs of {sdir.relative_to(ROOT)}/graph.json "
+                                   f"in {el:.1f} s across {cores} processes"},
         "e2e": {"value": round(v, 3), "unit": "inferences/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -488,12 +687,22 @@ def main(argv=None) -> int:
     ap.add_argument("--grids", default="auto", choices=["auto", "bounded", "full"],
                     help="bounded = size each conv for its DAG level's share of the SMs (Opara bounded "
                          "grids); full = whole GPU per conv; auto = build both, keep the faster Opara graph")
+    ap.add_argument("--cpu-model-seconds", type=float, default=3.0,
+                    help="budget of the PyTorch-eager CPU forward baseline (0 = skip)")
+    ap.add_argument("--save-schedule", default=None,
+                    help="directory for the timed graph's schedule files (default gpurun_out/schedules)")
     args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
-    line = run_reference(args) if args.impl == "reference" else run_gpu(args)
+    resolve_dtype(args)
+    if args.impl == "reference":
+        line, rc = run_reference(args), 0
+    else:
+        line, rc = run_gpu(args)
     if line is not None:
         print(json.dumps(line), flush=True)
-    return 0
+    if rc:
+        print("bench: the timed graph failed its parity gate (output tolerance or schedule)", file=sys.stderr)
+    return rc
 
 
 if __name__ == "__main__":

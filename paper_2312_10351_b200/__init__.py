@@ -8,7 +8,14 @@ with hand-written sm_100a kernels (``compile`` / ``ScheduledGraph.run``); the
 simulated run itself is kept as a bit-exact C++ port (``simulate``).
 """
 
-__version__ = "0.1.0"
+__version__ = "0.1.0"  # the reference opsched version this package is a drop-in for (cli metadata)
+
+import os as _os
+
+# The driver reads CUDA_DEVICE_MAX_CONNECTIONS once, when the CUDA context is
+# created: set it before any CUDA call so every plan stream can map onto its
+# own hardware queue (bench.py sets it before importing torch as well).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 from .dag import (ComputationGraph, OpClass, OperatorNode, ResourceDemand, apply_profile,
                   classify, graph_from_dict, graph_to_dict, load_graph, save_graph)
@@ -19,8 +26,8 @@ from .errors import (CoverageError, CudaError, FormatError, GraphValidationError
 from .order import (POLICIES, LaunchSchedule, ResourceScore, dominant_share, load_schedule,
                     make_order, order_baseline, order_opara, resource_score, save_schedule,
                     schedule_to_dict)
-from .plan import (DEFAULT_SYNC_OVERHEAD_US, PlanCost, StreamPlan, allocate_streams, load_plan,
-                   plan_to_dict, save_plan, single_stream_plan, validate_plan)
+from .plan import (DEFAULT_SYNC_OVERHEAD_US, PlanCost, StreamPlan, allocate_streams, evaluate_plan,
+                   load_plan, plan_to_dict, save_plan, single_stream_plan, validate_plan)
 from .simulator import (BlockRecord, OpRecord, SimResult, result_to_dict, sequential_makespan,
                         sequential_makespan_ns, simulate, trace, trace_tsv, write_trace)
 
@@ -29,7 +36,7 @@ __all__ = [
     "DEFAULT_SYNC_OVERHEAD_US", "FormatError", "GPU_PRESETS", "GpuConfig", "GraphValidationError",
     "InfeasibleBlockError", "LaunchSchedule", "OpClass", "OperatorNode", "POLICIES", "PlanCost",
     "PlanViolationError", "ResourceDemand", "ResourceScore", "SchedulerError", "StreamPlan",
-    "allocate_streams", "apply_profile", "classify", "device_gpu_config", "dominant_share",
+    "allocate_streams", "apply_profile", "evaluate_plan", "classify", "device_gpu_config", "dominant_share",
     "gpu_config_to_dict", "graph_from_dict", "graph_to_dict", "load_gpu_config", "load_graph",
     "load_plan", "load_schedule", "make_order", "order_baseline", "order_opara", "plan_to_dict",
     "resource_score", "save_graph", "save_plan", "save_schedule", "schedule_to_dict",

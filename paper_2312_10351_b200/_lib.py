@@ -126,7 +126,27 @@ def lib() -> C.CDLL:
             fn.restype = res
             fn.argtypes = args
         _lib = handle
+        _check_fresh(handle)
     return _lib
+
+
+def version() -> str:
+    return lib().opara_version().decode()
+
+
+def _check_fresh(handle) -> None:
+    """Refuse a libopara.so built from other sources than the ones next to it
+    (opara_version() carries the build's source hash, build.source_hash())."""
+    if os.environ.get("OPARA_ALLOW_STALE") == "1":
+        return
+    from . import build
+    if not build.CSRC.is_dir():
+        return
+    got = handle.opara_version().decode().rpartition("src:")[2]
+    want = build.source_hash()
+    if got != want:
+        raise ImportError(f"{_LIB_PATH} is stale: built from sources {got}, the tree has {want}; "
+                          "rebuild with `python -m paper_2312_10351_b200.build`")
 
 
 def check(status: int) -> None:

@@ -26,7 +26,7 @@ CSRC = PKG / "csrc"
 _FLAGS = os.environ.get("OPARA_NVCC_FLAGS", "")  # A/B experiments only: own object dir + relink
 BUILD = ROOT / "build" / ("opara" if not _FLAGS else "opara-" + hashlib.sha1(_FLAGS.encode()).hexdigest()[:8])
 LIB = PKG / "libopara.so"
-STAMP = BUILD.parent / "libopara.flags"
+STAMP = PKG / "libopara.hash"   # source hash of the linked libopara.so (travels with it)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", f"-I{ROOT / 'include'}", f"-I{CSRC}",
@@ -42,12 +42,27 @@ def _headers() -> list[Path]:
     return sorted([*CSRC.glob("*.h"), *CSRC.glob("*.cuh"), *(ROOT / "include").glob("*.h")])
 
 
-def _compile(src: Path, verbose: bool) -> Path:
+def source_hash() -> str:
+    """sha1 (12 hex) of every source and header the library is built from plus
+    the extra nvcc flags; embedded in opara_version() and checked on load."""
+    h = hashlib.sha1(_FLAGS.encode())
+    for f in _sources() + _headers():
+        h.update(f.name.encode() + b"\0" + f.read_bytes() + b"\0")
+    return h.hexdigest()[:12]
+
+
+def _compile(src: Path, verbose: bool, src_hash: str) -> Path:
     obj = BUILD / (src.name + ".o")
-    newest_dep = max([src.stat().st_mtime] + [h.stat().st_mtime for h in _headers()])
-    if obj.exists() and obj.stat().st_mtime >= newest_dep:
+    stamp = BUILD / (src.name + ".hash")
+    # content-addressed: an object is reused only if it was built from exactly
+    # these sources (mtimes lie after checkouts and snapshot copies)
+    key = src_hash if src.name == "sched.cpp" else hashlib.sha1(
+        b"".join(f.read_bytes() for f in [src] + _headers()) + _FLAGS.encode()).hexdigest()
+    if obj.exists() and stamp.exists() and stamp.read_text() == key:
         return obj
     cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
+    if src.name == "sched.cpp":
+        cmd.append(f'-DOPARA_SOURCE_HASH="{src_hash}"')
     if src.suffix == ".cu":
         cmd += ["-Xptxas", "-v"] if verbose else []
     else:
@@ -57,6 +72,7 @@ def _compile(src: Path, verbose: bool) -> Path:
         raise RuntimeError(f"nvcc failed on {src.name}:\n{res.stderr}")
     if verbose and res.stderr:
         (BUILD / (src.name + ".ptxas.txt")).write_text(res.stderr)
+    stamp.write_text(key)
     return obj
 
 
@@ -65,10 +81,10 @@ def build(verbose: bool = False, clean: bool = False) -> Path:
         shutil.rmtree(BUILD)
     BUILD.mkdir(parents=True, exist_ok=True)
     srcs = _sources()
+    src_hash = source_hash()
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as pool:
-        objs = list(pool.map(lambda s: _compile(s, verbose), srcs))
-    same_flags = STAMP.exists() and STAMP.read_text() == _FLAGS
-    if same_flags and LIB.exists() and LIB.stat().st_mtime >= max(o.stat().st_mtime for o in objs):
+        objs = list(pool.map(lambda s: _compile(s, verbose, src_hash), srcs))
+    if LIB.exists() and STAMP.exists() and STAMP.read_text() == src_hash:
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcuda"]
@@ -76,7 +92,7 @@ def build(verbose: bool = False, clean: bool = False) -> Path:
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
     os.replace(tmp, LIB)
-    STAMP.write_text(_FLAGS)
+    STAMP.write_text(src_hash)
     return LIB
 
 

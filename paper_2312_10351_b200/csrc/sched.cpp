@@ -200,7 +200,12 @@ std::vector<int32_t> order_wavefront(const opara_dag& g) {
 extern "C" {
 
 const char* opara_last_error(void) { return opara::g_last_error.c_str(); }
-const char* opara_version(void) { return "0.1.0 sm_100a"; }
+#ifndef OPARA_SOURCE_HASH
+#define OPARA_SOURCE_HASH "unknown"
+#endif
+// "<version> sm_100a src:<sha1 of every csrc/include source + nvcc flags>" (build.py
+// source_hash): ties a loaded binary to the sources it was built from.
+const char* opara_version(void) { return "0.1.0 sm_100a src:" OPARA_SOURCE_HASH; }
 
 opara_status opara_dag_create(const opara_node* nodes, int64_t n, const int64_t* edges_uv,
                               int64_t m, opara_dag** out) {

@@ -575,10 +575,11 @@ class ScheduledGraph:
                         seen.add(launch)
                         cands.append(rec)
                         owner.append((key, ("simt", var), sp, prof.num_blocks))
-                # narrow convs: the pixel-major tile (pixels on UMMA M, channels on N)
+                # narrow convs: the pixel-major 3xTF32 tile (pixels on UMMA M, channels on N);
+                # its weights are packed for the fp32 engine, so only fp32-engine convs qualify
                 cout = self.program.ops[k0].ints["Cout"]
                 for var, nw in ((4, 32), (5, 64)):
-                    if cout > nw:
+                    if cout > nw or recs[k0].i[22] != 1:
                         continue
                     t = torch.from_numpy(pack_conv_weights_tf32x3(self.program.ops[k0].weight, rows=nw)).to(self.dev)
                     self._keep.append(t)
@@ -588,6 +589,8 @@ class ScheduledGraph:
                     rec.p[1], rec.variant, rec.i[19] = px_w[(k0, var)], var, 0
                     prof = _lib.OparaOpProfile()
                     if L.opara_op_launch_config(C.byref(rec), C.byref(prof)) != 0:
+                        continue
+                    if budget and prof.num_blocks > max(budget, 8):
                         continue
                     cands.append(rec)
                     owner.append((key, ("px", var), 0, prof.num_blocks))
@@ -874,7 +877,10 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
     conv/GEMM's tile width and split-K by measurement (ScheduledGraph._autotune).
     splitk: split-K reduction ("push" / "pull" / "auto", see ScheduledGraph) for
     a fixed grid policy; default pull with bounded grids, push with full grids."""
-    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+    if torch.cuda.is_initialized() and int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")) < 32:
+        import warnings
+        warnings.warn("CUDA context created before CUDA_DEVICE_MAX_CONNECTIONS=32 was set: "
+                      "concurrent plan streams share fewer hardware queues", RuntimeWarning)
     program = lower(model, example, dtype, fuse_layernorm)
     if bound_grids != "auto":
         # measured default: pull reductions pair with bounded grids, push with full grids

@@ -408,12 +408,15 @@ class _Lowerer:
         lead = ins[0].shape[:-1]
         if any(t.shape[:-1] != lead for t in ins):
             raise LoweringError(f"{node.name}: concat inputs disagree outside the channel dim")
+        if any(t.dtype != ins[0].dtype for t in ins):
+            # COPY kernels move one element type; a converting copy does not exist
+            raise LoweringError(f"{node.name}: concat of mixed dtypes {sorted({t.dtype for t in ins})}")
         ctot = sum(t.shape[-1] for t in ins)
         out = self.new_tensor(tuple(lead) + (ctot,), dtype=ins[0].dtype)
         off = 0
         placed = []
         for p, t in zip(parts, ins):
-            if t.alias is not None or t.nchw_input or t.is_graph_input or t.dtype != out.dtype:
+            if t.alias is not None or t.nchw_input or t.is_graph_input:
                 t = self._copy_into(t, f"{node.name}.copy")
             t.alias = out
             t.coff_in_alias = off

@@ -193,6 +193,24 @@ def plan_cost(sequential_us: float, parallel_us: float, sync_count: int,
         exceeds_sequential=parallel_us > sequential_us)
 
 
+def evaluate_plan(g: ComputationGraph, plan: StreamPlan, order, cfg,
+                  sync_overhead_us: float = DEFAULT_SYNC_OVERHEAD_US) -> PlanCost:
+    """Eq. (1)-(3) cost of (plan, order) on the execution model (allocator.py:180-206):
+    the plan is validated first (PlanViolationError on any violation), then the
+    sequential and parallel makespans come from the C++ port of ``simulate``.
+    ``parallel_ratio`` above 1 is flagged by ``exceeds_sequential``, not clamped."""
+    from .simulator import sequential_makespan_ns, simulate   # simulator imports this module
+    require_valid(g, plan)
+    seq_ns = sequential_makespan_ns(g, cfg)
+    para_ns = simulate(g, plan, order, cfg).makespan_ns
+    count = len(plan.sync_events)
+    return PlanCost(sequential_us=seq_ns / 1000, parallel_us=para_ns / 1000,
+                    parallel_ratio=para_ns / seq_ns if seq_ns else 0.0,
+                    sync_count=count, sync_overhead_us=sync_overhead_us,
+                    total_us=para_ns / 1000 + count * sync_overhead_us,
+                    exceeds_sequential=para_ns > seq_ns)
+
+
 def require_valid(g: ComputationGraph, plan: StreamPlan) -> None:
     problems = validate_plan(g, plan)
     if problems:

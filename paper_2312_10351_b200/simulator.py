@@ -108,8 +108,9 @@ def simulate(g: ComputationGraph, plan: StreamPlan, schedule, cfg: GpuConfig, *,
              blocks: bool = True) -> SimResult:
     """Run the execution model for one (plan, launch order) pair.
 
-    ``blocks=False`` skips materialising the per-block log (the makespan and
-    every per-op field are unaffected)."""
+    ``blocks=False`` skips materialising the per-block log: the makespan, SM
+    busy times and every per-op timing field are unaffected, but ``OpRecord.sms``
+    (rebuilt from the block log) is empty and ``blocks`` is ``()``."""
     order = _order_of(schedule)
     _check_inputs(g, plan, order, cfg)
     if not order:

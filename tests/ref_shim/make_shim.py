@@ -25,22 +25,9 @@ ERRORS = "from paper_2312_10351_b200.errors import *  # noqa\n" \
          "    PlanViolationError, CoverageError, InfeasibleBlockError)\n"
 GRAPH = "from paper_2312_10351_b200.dag import (OpClass, classify, ResourceDemand, OperatorNode,\n" \
         "    ComputationGraph, load_graph, save_graph, graph_to_dict, apply_profile, _read_json)\n"
-ALLOCATOR = '''from paper_2312_10351_b200.plan import (DEFAULT_SYNC_OVERHEAD_US, PlanCost, StreamPlan,
-    allocate_streams, load_plan, plan_to_dict, save_plan, single_stream_plan, validate_plan,
-    plan_cost, require_valid)
-
-
-def evaluate_plan(g, plan, order, cfg, sync_overhead_us=DEFAULT_SYNC_OVERHEAD_US):
-    """Glue: our validation + plan_cost around the reference's simulated makespans."""
-    from .simulator import sequential_makespan_ns, simulate
-    require_valid(g, plan)
-    seq_ns = sequential_makespan_ns(g, cfg)
-    para_ns = simulate(g, plan, order, cfg).makespan_ns
-    cost = plan_cost(seq_ns / 1000, para_ns / 1000, len(plan.sync_events), sync_overhead_us)
-    return PlanCost(cost.sequential_us, cost.parallel_us,
-                    para_ns / seq_ns if seq_ns else 0.0, cost.sync_count,
-                    cost.sync_overhead_us, cost.total_us, para_ns > seq_ns)
-'''
+ALLOCATOR = "from paper_2312_10351_b200.plan import (DEFAULT_SYNC_OVERHEAD_US, PlanCost, StreamPlan,\n" \
+            "    allocate_streams, evaluate_plan, load_plan, plan_to_dict, save_plan, single_stream_plan,\n" \
+            "    validate_plan)\n"
 SIMULATOR = "from paper_2312_10351_b200.simulator import *  # noqa\n" \
             "from paper_2312_10351_b200.simulator import (BlockRecord, OpRecord, SimResult, TRACE_HEADER,\n" \
             "    DEFAULT_GPU, GPU_PRESETS, GpuConfig, gpu_config_to_dict, load_gpu_config, result_to_dict,\n" \

@@ -33,7 +33,11 @@ def test_library_exports_every_declared_symbol():
 
 def test_version_and_error_plumbing():
     L = _lib.lib()
-    assert L.opara_version().decode().startswith("0.1.0")
+    from paper_2312_10351_b200 import __version__, build
+    v = L.opara_version().decode()
+    assert v.startswith(__version__ + " sm_100a")
+    # provenance: the loaded binary was built from exactly the sources in the tree
+    assert v.rpartition("src:")[2] == build.source_hash()
     h = ctypes.c_void_p()
     st = L.opara_dag_create(None, -1, None, 0, ctypes.byref(h))
     assert st == 8 and b"bad arguments" in L.opara_last_error()
