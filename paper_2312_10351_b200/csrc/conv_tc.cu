@@ -79,6 +79,25 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Sum the 3xTF32 accumulators of this warp's lane quarter (hh, hl[, lh] at
+// columns c, BN + c, 2 BN + c) over its half of the BN pixel columns, 16
+// columns per step with every TMEM load in flight before one wait, and hand
+// each (column, sum) to `put`.  Summation order hh + (hl + lh) throughout.
+template <int BN, int kAcc, typename Put>
+__device__ __forceinline__ void drain_accumulators(uint32_t trow, int half, Put put) {
+  constexpr int kCols = BN / 2;   // two warps per lane quarter
+#pragma unroll 1
+  for (int c = half * kCols; c < (half + 1) * kCols; c += 16) {
+    float v[16], c1[16], c2[16];
+    if constexpr (kAcc == 3)
+      tc::tmem_ld16x3(trow + c, trow + BN + c, trow + 2 * BN + c, v, c1, c2);
+    else
+      tc::tmem_ld16x2(trow + c, trow + BN + c, v, c1);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) put(c + e, v[e] + (kAcc == 3 ? (c1[e] + c2[e]) : c1[e]));
+  }
+}
+
 template <int BN, bool kVec>
 __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsigned long long* trace) {
   constexpr int kStages = tc_stages(BN);
@@ -93,6 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   constexpr int kRowGroups = BN / 8;
   constexpr int kRowsPerThread = (kRowGroups + 3) / 4;  // atoms per gather/convert thread
   constexpr uint32_t kIdesc = tc::instr_desc(2, 128, BN);
+  constexpr uint32_t kIdesc2 = tc::instr_desc(2, 128, BN <= 128 ? 2 * BN : BN);   // hi*[hi; lo]
   // Separate TMEM accumulators for hi*hi, hi*lo and lo*hi: consecutive MMAs
   // then target different tiles and overlap in the tensor pipe instead of
   // serialising on one accumulator (BN = 256 shares one for both corrections).
@@ -311,11 +331,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   } else if (warp == kLoadWarp) {
     // ------------------------------------------------------------ weight loader
     if (lane == 0) {
+      // The CTA's whole weight slice is one contiguous run of packed stages.
+      // The ring holds kStages of them; the rest is requested into L2 now
+      // (before the predecessor has finished), so every later refill is an
+      // L2 hit instead of an HBM round trip (the k-loop was weight-latency bound).
+      const float* wslice = a.wpack + (static_cast<int64_t>(mt) * a.kblocks + kb0) * (2 * kWBytes / 4);
+      if (nkb > kStages)
+        tc::bulk_prefetch_l2(wslice + static_cast<int64_t>(kStages) * (2 * kWBytes / 4),
+                             static_cast<uint64_t>(nkb - kStages) * 2 * kWBytes);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
         tc::mbar_arrive_expect_tx(&full[s], 2 * kWBytes);
-        const float* src = a.wpack + (static_cast<int64_t>(mt) * a.kblocks + kb0 + i) * (2 * kWBytes / 4);
+        const float* src = wslice + static_cast<int64_t>(i) * (2 * kWBytes / 4);
         tc::bulk_g2s(smem + s * kStage, src, 2 * kWBytes, &full[s]);
       }
     }
@@ -334,11 +362,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
         const uint64_t ah = tc::smem_desc_sw64(w_hi + 32 * ks, kSbo);
         const uint64_t al = tc::smem_desc_sw64(w_lo + 32 * ks, kSbo);
         const uint64_t bh = tc::smem_desc_sw64(x_hi + 32 * ks, kSbo);
-        const uint64_t bl = tc::smem_desc_sw64(x_lo + 32 * ks, kSbo);
         const uint32_t first = (i | ks) != 0;
-        tc::mma_tf32(tmem, ah, bh, kIdesc, first);
-        tc::mma_tf32(tmem + BN, ah, bl, kIdesc, first);
-        tc::mma_tf32(tmem + (kAcc - 1) * BN, al, bh, kIdesc, kAcc == 3 ? first : 1u);
+        if constexpr (kAcc == 3) {
+          // The lo plane's atoms follow the hi plane's (x_lo = x_hi + BN/8
+          // atoms at the same SBO), so one N = 2 BN MMA computes hi*hi
+          // (columns [0, BN)) and hi*lo ([BN, 2 BN)) reading the W hi tile
+          // once: the tf32 MMAs are shared-memory-bandwidth bound.
+          tc::mma_tf32(tmem, ah, bh, kIdesc2, first);
+          tc::mma_tf32(tmem + 2 * BN, al, bh, kIdesc, first);
+        } else {
+          const uint64_t bl = tc::smem_desc_sw64(x_lo + 32 * ks, kSbo);
+          tc::mma_tf32(tmem, ah, bh, kIdesc, first);
+          tc::mma_tf32(tmem + BN, ah, bl, kIdesc, first);
+          tc::mma_tf32(tmem + BN, al, bh, kIdesc, 1u);
+        }
       }
       tc::mma_commit(&empty[s]);
     }
@@ -365,20 +402,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       const int quarter = warp & 3, half = warp >> 2;
       const int chl = quarter * 32 + lane;
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-      constexpr int kC8 = BN / 8 / (kProducerWarps / 4);
-#pragma unroll 2
-      for (int c8 = half * kC8; c8 < (half + 1) * kC8; ++c8) {
-        float v[8], c1[8], c2[8];
-        tc::tmem_ld8(trow + c8 * 8, v);
-        tc::tmem_ld8(trow + BN + c8 * 8, c1);
-        if constexpr (kAcc == 3) tc::tmem_ld8(trow + 2 * BN + c8 * 8, c2);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int col = c8 * 8 + e, owner = col / rp;
-          stage[(owner * rp + (col - owner * rp)) * 128 + chl] = v[e] + (kAcc == 3 ? (c1[e] + c2[e]) : c1[e]);
-        }
-      }
+      // the owner blocks are [rows_per cols][128 ch] back to back: column col
+      // lands at stage[col * 128 + channel] whatever its owner
+      drain_accumulators<BN, kAcc>(trow, half, [&](int col, float val) { stage[col * 128 + chl] = val; });
       tc::fence_proxy_async_smem();   // generic-proxy writes -> the bulk copy engine
+      DBG(4);
     }
     tc::tc_fence_before();
     // push: the owners' receive buffers sit behind their rings (always free);
@@ -406,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     const int ch = mt * 128 + tid;
     if (mine > 0 && tid < 128 && ch < a.Cout) {
       tc::mbar_wait_cluster(rbar, 0);
+      DBG(5);
       for (int c0 = 0; c0 < mine; c0 += 4) {   // recv = [src rank][rows_per cols][128 ch]
         float part[kMaxSplits][4];               // every load of 4 columns issued before the adds
 #pragma unroll
@@ -424,7 +453,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
         }
       }
     }
+    DBG(6);
     if (tid == 0) tc::bulk_wait_read();   // the source blocks stay valid until the engine has read them
+    DBG(7);
     trace_end(trace);
     return;
   }
@@ -437,21 +468,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     DBG(4);
     const int quarter = warp & 3, half = warp >> 2;
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    constexpr int kC8 = BN / 8 / (kProducerWarps / 4);
-#pragma unroll 4
-    for (int c8 = half * kC8; c8 < (half + 1) * kC8; ++c8) {
-      float v[8];
-      tc::tmem_ld8(trow + c8 * 8, v);
-      {
-        float c1[8], c2[8];
-        tc::tmem_ld8(trow + BN + c8 * 8, c1);
-        if constexpr (kAcc == 3) tc::tmem_ld8(trow + 2 * BN + c8 * 8, c2);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] += kAcc == 3 ? (c1[e] + c2[e]) : c1[e];
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) tile[(c8 * 8 + e) * 128 + quarter * 32 + lane] = v[e];
-    }
+    drain_accumulators<BN, kAcc>(trow, half,
+                                 [&](int col, float val) { tile[col * 128 + quarter * 32 + lane] = val; });
   }
   tc::tc_fence_before();
   const int splits = a.splits;
@@ -690,6 +708,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3_px(TcArgs a, uns
     }
   } else if (warp == kLoadWarp) {
     if (lane == 0) {
+      if (nkb > kPxStages)   // the rest of the weight stream into L2 (see the channel-major kernel)
+        tc::bulk_prefetch_l2(a.wpack + static_cast<int64_t>(kPxStages) * (2 * kWB / 4),
+                             static_cast<uint64_t>(nkb - kPxStages) * 2 * kWB);
       for (int i = 0; i < nkb; ++i) {
         const int st = i % kPxStages;
         if (i >= kPxStages) tc::mbar_wait(&empty[st], ((i / kPxStages) - 1) & 1);

@@ -430,11 +430,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     }
   } else if (warp == kLoadWarp) {
     if (lane == 0) {
+      // ring refills beyond the first kStages come from L2: request the rest of
+      // the CTA's contiguous weight slice now, before the predecessor finishes
+      const __nv_bfloat16* wslice = a.wpack + (static_cast<int64_t>(mt) * a.kblocks + kb0) * (kWBytes / 2);
+      if (nkb > kStages)
+        tc::bulk_prefetch_l2(wslice + static_cast<int64_t>(kStages) * (kWBytes / 2),
+                             static_cast<uint64_t>(nkb - kStages) * kWBytes);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
         tc::mbar_arrive_expect_tx(&full[s], kWBytes);
-        const __nv_bfloat16* src = a.wpack + (static_cast<int64_t>(mt) * a.kblocks + kb0 + i) * (kWBytes / 2);
+        const __nv_bfloat16* src = wslice + static_cast<int64_t>(i) * (kWBytes / 2);
         tc::bulk_g2s(smem + s * kStage, src, kWBytes, &full[s]);
       }
     }

@@ -18,6 +18,7 @@ ap.add_argument("dtype", nargs="?", default="f32")
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--grids", default="auto")
 args = ap.parse_args()
+bench.resolve_dtype(args)
 model, _, x = bench.build_workload(args)
 sg = engine.compile(model, x, device=0, dtype=args.dtype,
                     bound_grids={"auto": "auto", "bounded": True, "full": False}[args.grids])
