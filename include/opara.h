@@ -17,6 +17,8 @@
  *   opara_dominant_share      dominant_share                      orderer.py:45-53
  *   opara_order               order_opara (Alg. 2) / order_baseline("sequential"|"dfs"|
  *                             "wavefront")                        orderer.py:60-153
+ *   opara_linear_extensions   oracle.linear_extensions (every launch
+ *                             order, lexicographic by id)         oracle.py:52-84
  *   opara_simulate            simulate (the reference "run": DES model),
  *                             bit-exact C++ port                  simulator.py:212-415
  *   opara_exec_*              the same "run" re-designed as a real multi-stream
@@ -137,6 +139,14 @@ opara_status opara_dominant_share(const opara_node* node, const opara_gpu_config
 /* Launch order (n node ids).  cfg may be NULL for the non-opara policies. */
 opara_status opara_order(const opara_dag* dag, int32_t policy, const opara_gpu_config* cfg,
                          int64_t* out);
+
+/* Every linear extension of the DAG in lexicographic order by node id (the
+ * enumeration order of oracle.linear_extensions, oracle.py:52-84).  Skips the
+ * first `skip` extensions, then writes up to `cap` orders of n ids each into
+ * out[cap][n]; *written receives the number written and *exhausted 1 when the
+ * enumeration ended inside this call (no extension after the last written). */
+opara_status opara_linear_extensions(const opara_dag* dag, int64_t skip, int64_t cap, int64_t* out,
+                                     int64_t* written, int32_t* exhausted);
 
 /* -------------------------------------------- execution model (L4) */
 

@@ -379,6 +379,48 @@ def simulate_makespan_ns(g: Dag, assignment, num_streams, sync, order, cfg):
     return max(done_at.values())
 
 
+# ------------------------------------------------------ exhaustive search
+
+
+def linear_extensions(g: Dag):
+    """Every linear extension, lexicographic by id (oracle.py:52-84)."""
+    indeg = {v: len(g.pred[v]) for v in g.ids}
+    prefix = []
+
+    def walk():
+        if len(prefix) == len(g.ids):
+            yield tuple(prefix)
+            return
+        for v in [u for u in g.ids if indeg[u] == 0 and u not in placed]:
+            placed.add(v)
+            prefix.append(v)
+            for s in g.succ[v]:
+                indeg[s] -= 1
+            yield from walk()
+            for s in g.succ[v]:
+                indeg[s] += 1
+            prefix.pop()
+            placed.discard(v)
+
+    placed = set()
+    yield from walk()
+
+
+def best_order(g: Dag, assignment, num_streams, sync, cfg, limit=None):
+    """(best makespan ns, best order, examined, exhausted) — first minimum wins
+    (oracle.py:87-122)."""
+    best_ns, best, examined, exhausted = None, (), 0, True
+    for order in linear_extensions(g):
+        if limit is not None and examined >= limit:
+            exhausted = False
+            break
+        examined += 1
+        ns = simulate_makespan_ns(g, assignment, num_streams, sync, list(order), cfg)
+        if best_ns is None or ns < best_ns:
+            best_ns, best = ns, order
+    return (0 if best_ns is None else best_ns), best, examined, exhausted
+
+
 # ------------------------------------------------------------------ helpers
 
 

@@ -93,6 +93,7 @@ SIGNATURES = {
     "opara_dominant_share": (C.c_int, [C.POINTER(OparaNode), C.POINTER(OparaGpuConfig),
                                        C.POINTER(C.c_double)]),
     "opara_order": (C.c_int, [_P, C.c_int32, C.POINTER(OparaGpuConfig), _P]),
+    "opara_linear_extensions": (C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P]),
     "opara_simulate": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, C.c_int64, C.POINTER(OparaGpuConfig),
                                  C.POINTER(OparaSimResult), _P, _P, _P, _P, C.c_int64, _I64P]),
     "opara_exec_create": (C.c_int, [C.c_int32, _P, C.c_int64, C.POINTER(_P)]),

@@ -463,4 +463,50 @@ opara_status opara_order(const opara_dag* g, int32_t policy, const opara_gpu_con
   return OPARA_OK;
 }
 
+// Depth-first walk over ready sets kept sorted ascending, so extensions come
+// out in lexicographic id order (oracle.py:52-84 enumerates the same way).
+opara_status opara_linear_extensions(const opara_dag* g, int64_t skip, int64_t cap, int64_t* out,
+                                     int64_t* written, int32_t* exhausted) {
+  if (!g || !written || !exhausted || (cap > 0 && !out) || skip < 0 || cap < 0)
+    return fail(OPARA_ERR_VALUE, "null argument");
+  const int32_t n = g->n();
+  std::vector<int32_t> indeg(n);
+  for (int32_t v = 0; v < n; ++v) indeg[v] = g->pred_off[v + 1] - g->pred_off[v];
+  std::vector<int32_t> prefix;
+  prefix.reserve(n);
+  std::vector<char> used(n, 0);
+  int64_t seen = 0, nw = 0;
+  bool stop = false;
+  // ready set = {v : !used[v] && indeg[v] == 0}; scanning v ascending is the
+  // lexicographic branch order (n is tiny: the space is up to n!)
+  auto walk = [&](auto&& self) -> void {
+    if (static_cast<int32_t>(prefix.size()) == n) {
+      if (seen++ >= skip) {
+        if (nw == cap) {
+          stop = true;
+          return;
+        }
+        for (int32_t k = 0; k < n; ++k) out[nw * n + k] = g->id(prefix[k]);
+        ++nw;
+      }
+      return;
+    }
+    for (int32_t v = 0; v < n && !stop; ++v) {
+      if (used[v] || indeg[v]) continue;
+      used[v] = 1;
+      prefix.push_back(v);
+      for (int32_t e = g->succ_off[v]; e < g->succ_off[v + 1]; ++e) --indeg[g->succ[e]];
+      self(self);
+      for (int32_t e = g->succ_off[v]; e < g->succ_off[v + 1]; ++e) ++indeg[g->succ[e]];
+      prefix.pop_back();
+      used[v] = 0;
+    }
+  };
+  if (cap > 0 || n == 0) walk(walk);
+  else stop = true;
+  *written = nw;
+  *exhausted = stop ? 0 : 1;
+  return OPARA_OK;
+}
+
 }  // extern "C"

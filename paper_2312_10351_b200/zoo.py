@@ -46,9 +46,52 @@ MODELS = {
 }
 
 
+def _block(make):
+    def fn(seed: int = 0) -> nn.Module:
+        torch.manual_seed(seed)
+        m = make()
+        for mod in m.modules():
+            if isinstance(mod, nn.Conv2d):
+                nn.init.kaiming_normal_(mod.weight, nonlinearity="relu")
+        _randomise_bn(m, torch.Generator().manual_seed(seed + 1))
+        return m.eval()
+    return fn
+
+
+def _googlenet_3a():
+    from torchvision.models.googlenet import Inception
+    return Inception(192, 64, 96, 128, 16, 32, 32)
+
+
+def _inception_a():
+    from torchvision.models.inception import InceptionA
+    return InceptionA(192, pool_features=32)
+
+
+def _inception_b():
+    from torchvision.models.inception import InceptionB
+    return InceptionB(288)
+
+
+def _inception_e():
+    from torchvision.models.inception import InceptionE
+    return InceptionE(1280)
+
+
+# Tiny sub-DAGs (one multi-branch block each) for the exhaustive launch-order
+# search measured on the GPU: the block's input is the
+# NCHW activation the full network feeds it.
+BLOCKS = {
+    "googlenet_3a": (_block(_googlenet_3a), (1, 192, 28, 28)),
+    "inception_v3_a": (_block(_inception_a), (1, 192, 35, 35)),
+    "inception_v3_b": (_block(_inception_b), (1, 288, 35, 35)),
+    "inception_v3_e": (_block(_inception_e), (1, 1280, 8, 8)),
+}
+
+
 def build(name: str, batch: int = 1, seed: int = 0):
-    """(model, example input) for a named config."""
-    fn, shape = MODELS[name]
+    """(model, example input) for a named config (or a sub-DAG block of BLOCKS)."""
+    fn, shape = MODELS[name] if name in MODELS else BLOCKS[name]
     model = fn(seed)
     g = torch.Generator().manual_seed(seed + 2)
     x = torch.randn((batch,) + tuple(shape[1:]), generator=g)

@@ -5,7 +5,8 @@ The reference test suite (/root/reference/pkg/tests, 158 tests) imports
 
 * errors / graph / allocator / orderer / simulator  ->  paper_2312_10351_b200
   (C++ via the C ABI: scheduler, and the bit-exact port of the execution model)
-* oracle / generators / cli / __init__ / __main__  ->  the reference modules
+* oracle  ->  paper_2312_10351_b200.search (exhaustive order / plan search)
+* generators / cli / __init__ / __main__  ->  the reference modules
   themselves (symlinked into a temp dir, never copied into the repo); they are
   out of the hot path and are the consumers of our outputs.
 
@@ -33,6 +34,8 @@ SIMULATOR = "from paper_2312_10351_b200.simulator import *  # noqa\n" \
             "    DEFAULT_GPU, GPU_PRESETS, GpuConfig, gpu_config_to_dict, load_gpu_config, result_to_dict,\n" \
             "    sequential_makespan, sequential_makespan_ns, simulate, trace, trace_tsv, write_trace,\n" \
             "    _check_inputs, _order_of)\n"
+ORACLE = "from paper_2312_10351_b200.search import (OracleResult, PlanSearchResult, linear_extensions,\n" \
+         "    best_order, best_plan, _partitions)\n"
 ORDERER = "from paper_2312_10351_b200.order import (POLICIES, LaunchSchedule, ResourceScore,\n" \
           "    dominant_share, resource_score, order_opara, order_baseline, make_order,\n" \
           "    schedule_to_dict, save_schedule, load_schedule)\n" \
@@ -47,7 +50,8 @@ def make_shim(root: Path) -> Path:
     (pkg / "allocator.py").write_text(ALLOCATOR)
     (pkg / "orderer.py").write_text(ORDERER)
     (pkg / "simulator.py").write_text(SIMULATOR)
-    for name in ("__init__.py", "__main__.py", "oracle.py", "generators.py", "cli.py"):
+    (pkg / "oracle.py").write_text(ORACLE)
+    for name in ("__init__.py", "__main__.py", "generators.py", "cli.py"):
         link = pkg / name
         if not link.exists():
             os.symlink(REF_SRC / name, link)

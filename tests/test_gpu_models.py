@@ -96,7 +96,7 @@ def test_bert_base_bf16_parity():
     assert _rel(pooled.float().reshape(ref_p.shape), ref_p) < 1e-2
 
 
-@pytest.mark.parametrize("dtype,tol", [("f32", 1e-4), ("bf16", 2e-2)])
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-4), ("bf16", 1e-2)])
 def test_nasnet_large_parity(dtype, tol):
     """NASNet-A Large 331x331 (~700 kernels, ~160 plan streams) through the
     scheduled graph vs the fp32 eager forward."""

@@ -59,9 +59,9 @@ class SepBlock(nn.Module):
 
 @pytest.mark.parametrize("c,k,s,hw,dtype,tol", [(32, 3, 1, 21, "f32", 1e-4), (48, 5, 2, 42, "f32", 1e-4),
                                                 (64, 7, 2, 83, "f32", 1e-4), (40, 3, 1, 11, "f32", 1e-4),
-                                                (64, 5, 2, 42, "bf16", 2e-2), (96, 7, 1, 21, "bf16", 2e-2),
-                                                (42, 5, 2, 83, "bf16", 2e-2), (84, 7, 2, 42, "bf16", 2e-2),
-                                                (42, 3, 1, 21, "f32", 1e-4), (36, 5, 1, 11, "bf16", 2e-2)])
+                                                (64, 5, 2, 42, "bf16", 1e-2), (96, 7, 1, 21, "bf16", 1e-2),
+                                                (42, 5, 2, 83, "bf16", 1e-2), (84, 7, 2, 42, "bf16", 1e-2),
+                                                (42, 3, 1, 21, "f32", 1e-4), (36, 5, 1, 11, "bf16", 1e-2)])
 def test_separable_block(c, k, s, hw, dtype, tol):
     from paper_2312_10351_b200 import engine
     torch.manual_seed(0)
@@ -105,7 +105,7 @@ class ReluConvHead(nn.Module):
 
 
 @pytest.mark.parametrize("c,cout,hw,dtype,tol", [(64, 128, 21, "f32", 1e-4), (96, 64, 42, "f32", 1e-4),
-                                                 (64, 128, 21, "bf16", 2e-2), (128, 256, 11, "bf16", 2e-2)])
+                                                 (64, 128, 21, "bf16", 1e-2), (128, 256, 11, "bf16", 1e-2)])
 def test_relu_in_and_subsample(c, cout, hw, dtype, tol):
     from paper_2312_10351_b200 import engine
     torch.manual_seed(1)
@@ -120,10 +120,11 @@ def test_relu_in_and_subsample(c, cout, hw, dtype, tol):
     assert _rel(y, ref) <= tol
 
 
-@pytest.mark.parametrize("batch", [1, 8, 32])
+@pytest.mark.parametrize("batch", [1, 2, 4, 8, 16, 32])
 def test_deepfm_parity(batch):
+    """The BASELINE DeepFM batch sweep 1-32 at the bench's 100k-row vocab per field."""
     from paper_2312_10351_b200 import engine, zoo
-    model, (dense, ids) = zoo.build_deepfm(batch, vocab=20_000)
+    model, (dense, ids) = zoo.build_deepfm(batch)
     sg = engine.compile(model, (dense, ids), device=0, profile_reps=2)
     y = sg.run((dense.cuda(), ids.cuda()))
     y_seq = sg.run((dense.cuda(), ids.cuda()), slot=engine.SLOT_SEQUENTIAL)

@@ -43,3 +43,7 @@ def test_reference_suite_passes_against_native_scheduler(tmp_path):
         [sys.executable, "-c", "import opsched.simulator as s; print(s.simulate.__module__)"],
         capture_output=True, text=True, env=env, cwd=tmp_path)
     assert probe.stdout.strip() == "paper_2312_10351_b200.simulator", probe.stderr
+    probe = subprocess.run(
+        [sys.executable, "-c", "import opsched.oracle as o; print(o.best_order.__module__, o.linear_extensions.__module__)"],
+        capture_output=True, text=True, env=env, cwd=tmp_path)
+    assert probe.stdout.split() == ["paper_2312_10351_b200.search"] * 2, probe.stderr

@@ -51,3 +51,54 @@ def test_two_replicas_schedule_identically_and_time_is_max():
     assert res[0][1:3] == res[1][1:3] == (28, res[0][2])
     assert res[0][3] == res[1][3] == 2.0
     assert res[0][4] == res[1][4] == (True, "pull", 1.5)
+
+
+class _FakeGraph:
+    def __init__(self, variant, cache):
+        self.bound_grids, self.splitk, self.bound_scale = variant
+        self.cache = cache
+
+
+def _compile_worker(rank, world, port, tmp, q):
+    """bench.replica_compile's control flow with the device work stubbed: rank 0
+    searches (and writes its tile choices to its own tuning cache), every other
+    rank receives the variant + cache CONTENTS and builds exactly that."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import json
+    from pathlib import Path
+
+    import bench
+    calls = []
+
+    def search(cache_path):
+        calls.append("search")
+        Path(cache_path).write_text(json.dumps({"conv_17": [2, 64, 3]}))
+        return _FakeGraph((True, "pull", 1.5), cache_path)
+
+    def build_choice(variant, cache_path):
+        calls.append("build")
+        return _FakeGraph(variant, cache_path)
+
+    rank_dir = os.path.join(tmp, f"r{rank}")   # per-rank local temp dirs (multi-node safe)
+    os.makedirs(rank_dir, exist_ok=True)
+    sg, variant = bench.replica_compile(dist, rank, world, search, build_choice, rank_dir)
+    t = bench.time_max(dist, world, [0.5 + rank, 2.0 - rank])
+    q.put((rank, calls, variant, json.loads(Path(sg.cache).read_text()), t))
+    dist.destroy_process_group()
+
+
+def test_replica_compile_hands_rank0_choice_to_every_rank(tmp_path):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_compile_worker, args=(r, 2, port, str(tmp_path), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0][1] == ["search"] and res[1][1] == ["build"]
+    assert res[0][2] == res[1][2] == (True, "pull", 1.5)
+    assert res[0][3] == res[1][3] == {"conv_17": [2, 64, 3]}
+    assert res[0][4] == res[1][4] == [1.5, 2.0]
