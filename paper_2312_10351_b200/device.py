@@ -42,6 +42,10 @@ GPU_PRESETS: dict[str, GpuConfig] = {
     # cudaGetDeviceProperties on a B200 (sm_100): 148 SMs, 2048 threads,
     # 228 KiB smem, 64 Ki registers, 32 resident blocks per SM.
     "b200": GpuConfig(148, 2048, 233472, 65536, 32),
+    # same capacities, same-class slowdown fitted to measured B200 graph
+    # latencies of the seven block-bound BASELINE configs (scripts/calibrate.py,
+    # profiles/r02_calibration.md: mean |log error| 0.065 vs 0.102 at 1.4)
+    "b200-calibrated": GpuConfig(148, 2048, 233472, 65536, 32, 1.9),
 }
 
 DEFAULT_GPU = "2080s-like"
