@@ -74,3 +74,20 @@ for k in [r[0] for r in rows][:: max(1, len(rows) // 6)]:
     print(f"op {k}: issue  " + " ".join(f(d[768 + i]) for i in range(24) if d[768 + i]))
     print(f"op {k}: landed " + " ".join(f(d[256 + i]) for i in range(24) if d[256 + i]))
     print(f"op {k}: mma    " + " ".join(f(d[512 + i]) for i in range(24) if d[512 + i]))
+
+# hand-off between consecutive convs of the (sequential) replay: the previous
+# conv's last CTA exit (first 96 CTAs recorded) -> this conv's first CTA entry,
+# its setup done, its first gather issue (after griddepcontrol.wait) and first landed stage
+print("\nhand-off (us): prev last exit -> entry0 / setup0 / gather0 / land0   (negative = before the predecessor ended)")
+prev = None
+for k, buf in sorted(sg.debug_ts.items()):
+    d = buf.cpu().numpy().astype(np.int64)
+    if sg.engines.get(k) != 1 or d[0] == 0:
+        continue
+    ent = [d[64 + 2 * c] for c in range(96) if d[64 + 2 * c]]
+    ext = [d[65 + 2 * c] for c in range(96) if d[65 + 2 * c]]
+    if prev is not None and prev[0] == k - 1:
+        pe = prev[1]
+        print(f"{k:4d} {(min(ent) - pe) / 1e3:7.2f} {(d[1] - pe) / 1e3:7.2f} {(d[768] - pe) / 1e3:7.2f} "
+              f"{(d[256] - pe) / 1e3:7.2f}   last-CTA exit spread {(max(ext) - min(ext)) / 1e3:6.2f}")
+    prev = (k, max(ext) if ext else d[0])

@@ -90,8 +90,11 @@ void run(long long* d, int vary = 0) {
 int main() {
   long long* d;
   cudaMalloc(&d, 64);
-  for (int v = 0; v < 4; ++v) {
+  for (int v = 0; v < 4; v += 3) {
     run<2, 128, 32, 4>(d, v); run<2, 128, 64, 4>(d, v); run<2, 128, 128, 4>(d, v); run<2, 128, 256, 4>(d, v);
+    run<2, 128, 64, 2>(d, v); run<2, 128, 128, 2>(d, v); run<2, 128, 256, 2>(d, v);
+    run<2, 128, 64, 6>(d, v); run<2, 128, 128, 6>(d, v);
+    run<2, 128, 64, 0>(d, v); run<2, 128, 128, 0>(d, v);
     run<1, 128, 64, 4>(d, v); run<1, 128, 128, 4>(d, v); run<1, 128, 256, 4>(d, v); run<1, 128, 256, 2>(d, v);
   }
   return 0;
