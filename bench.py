@@ -429,6 +429,14 @@ def run_gpu(args) -> tuple[dict | None, int]:
     for slot, pol in ((10, "dfs"), (11, "wavefront")):
         sg.capture(slot, sg.plan, make_order(sg.graph, pol, sg.gpu_config))
         orders[pol] = round(sg.time(slot, warmup=args.warmup, iters=args.steps, flush_l2=True).median_ms, 4)
+    # diagnostic (not a reference policy): longest-remaining-path-first list order
+    # over the profiled kernel times, the order the B200 sub-DAG search favours
+    from paper_2312_10351_b200.order import LaunchSchedule
+    from paper_2312_10351_b200.search import critical_path_first_order
+    cpf = critical_path_first_order(sg.graph, {v: sg.profile[v - 1]["isolated_us"] for v in sg.graph.node_ids})
+    sg.capture(12, sg.plan, LaunchSchedule(cpf, "critical_path_first"))
+    orders["critical_path_first"] = round(sg.time(12, warmup=args.warmup, iters=args.steps,
+                                                  flush_l2=True).median_ms, 4)
 
     # e2e through the public API: pinned host in -> H2D -> replay -> D2H output
     e2e = sg.time_host_roundtrip(x, warmup=args.warmup, iters=args.steps)

@@ -51,15 +51,8 @@ constexpr uint32_t kWBytes = 128 * kBKF * 4;  // one precision plane of the W st
 
 // Ring depth per pixel tile: the small tiles keep the CTA under ~113 KB so two
 // CTAs (two concurrent branches) can share an SM.
-#ifndef OPARA_TC_STAGES_32
-#define OPARA_TC_STAGES_32 5
-#endif
-#ifndef OPARA_TC_STAGES_64
-#define OPARA_TC_STAGES_64 4
-#endif
-__host__ __device__ constexpr int tc_stages(int bn) {
-  return bn == 32 ? OPARA_TC_STAGES_32 : bn == 64 ? OPARA_TC_STAGES_64 : bn == 128 ? 6 : 4;
-}
+// (deeper rings measured neutral: the k loop is paced by the tensor pipe)
+__host__ __device__ constexpr int tc_stages(int bn) { return bn == 32 ? 5 : bn == 64 ? 4 : bn == 128 ? 6 : 4; }
 
 struct TcArgs {
   const float* __restrict__ in;
@@ -153,7 +146,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   const int mt = blockIdx.y;        // 128-channel tile
   const int kb0 = blockIdx.z * a.kb_per_split;
   const int nkb = min(a.kblocks, kb0 + a.kb_per_split) - kb0;
-#ifndef OPARA_BIAS_LATE
   // pull-epilogue bias (lane = 4 channels): a parameter, fetched before griddepcontrol.wait
   const int ch = mt * 128 + lane * 4;
   float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -163,7 +155,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     if (ch + 2 < a.Cout) bias4.z = __ldg(a.bias + ch + 2);
     if (ch + 3 < a.Cout) bias4.w = __ldg(a.bias + ch + 3);
   }
-#endif
   // push-epilogue owner reduction: thread = output channel
   const float push_bias = ((a.push || a.splits > 1) && a.bias && tid < 128 && mt * 128 + tid < a.Cout) ? __ldg(a.bias + mt * 128 + tid) : 0.f;
 
@@ -171,16 +162,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   uint64_t* rbar = accum + 2;
   float* recv = reinterpret_cast<float*>(smem + kStages * kStage + 512);
   const bool push = a.push != 0;
-  // Opt-in (-DOPARA_RING_PULL) pull-mode split-K without DSMEM loads: after one
-  // cluster barrier every rank bulk-copies its staged blocks into the owners'
-  // (now idle) rings.  Measured slower than the DSMEM pull in graphs
-  // (GoogLeNet fp32 0.234 -> 0.246 ms, BERT 0.482 -> 0.485 ms), so off by default.
-  const uint32_t stage_bytes = static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4);
-#ifndef OPARA_RING_PULL
-  const bool ring = false;
-#else
-  const bool ring = !push && a.splits > 1 && 2 * stage_bytes <= kStages * kStage;
-#endif
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], 32 * (kProducerWarps / 2) + 1);  // converters + the weight loader
@@ -188,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(accum, 1);
-    if (push || ring) tc::mbar_init(rbar, 1);
+    if (push) tc::mbar_init(rbar, 1);
     tc::fence_barrier_init();
   }
   // TMEM is allocated and freed by the MMA warp: idle in every epilogue
@@ -198,13 +179,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
     tc::cluster_sync();
     if (tid == 0) {   // every rank bulk-copies one whole [rows_per][128] block to each owner
       const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
-      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4));
+      // every other rank's block; the owner's own partial stays in its ring
+      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((a.splits - 1) * a.rows_per * 128 * 4));
     }
   } else {
-    if (ring && tid == 0) {   // owners expect every rank's block (the epilogue's cluster barrier orders it)
-      const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
-      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, stage_bytes);
-    }
     __syncthreads();
   }
   tc::tc_fence_after();
@@ -396,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   // TMEM -> [BN][128] fp32 tile in the idle pipeline smem (all MMAs, hence all
   // smem reads by the tensor core, are complete once `accum` fires).
   DBG(3);
-  if (push || ring) {
+  if (push) {
     // TMEM -> registers (sum of the 3xTF32 accumulators) -> this CTA's idle ring
     // smem as one contiguous [rows_per cols][128 ch] block per owning rank;
     // one thread bulk-copies each block into its owner's receive slot (TMA
@@ -417,20 +395,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       DBG(4);
     }
     tc::tc_fence_before();
-    // push: the owners' receive buffers sit behind their rings (always free);
-    // ring: they are the owners' rings past the staged blocks, free once every
-    // rank has drained its accumulators, i.e. after one cluster barrier
-    float* rbuf = push ? recv : reinterpret_cast<float*>(smem + stage_bytes);
-    if (ring)
-      tc::cluster_sync();
-    else
-      __syncthreads();
+    // the owners' receive buffers sit behind their rings (always free)
+    float* rbuf = recv;
+    __syncthreads();
     if (tid == 0) {
       const uint32_t block = static_cast<uint32_t>(128 * rp * 4);
       const uint32_t rbar_s = tc::smem_u32(rbar), recv_s = tc::smem_u32(rbuf), stage_s = tc::smem_u32(stage);
       for (int o = 0; o < a.splits && o * rp < BN; ++o)
-        tc::bulk_s2cluster(tc::map_cluster(recv_s + me * block, o), stage_s + o * block, block,
-                           tc::map_cluster(rbar_s, o));
+        if (o != static_cast<int>(me))
+          tc::bulk_s2cluster(tc::map_cluster(recv_s + me * block, o), stage_s + o * block, block,
+                             tc::map_cluster(rbar_s, o));
       tc::bulk_commit();
     }
     if (warp == kMmaWarp) {
@@ -449,7 +423,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
         for (int z = 0; z < kMaxSplits; ++z)
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (z < a.splits) part[z][e] = rbuf[(z * rp + c0 + e) * 128 + tid];
+            if (z < a.splits) part[z][e] = z == static_cast<int>(me) ? stage[(r0 + c0 + e) * 128 + tid]
+                                                                      : rbuf[(z * rp + c0 + e) * 128 + tid];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float acc = part[0][e];
@@ -496,16 +471,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   const int rank = splits > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
   const int rows_per = (BN + splits - 1) / splits;
   const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
-#ifdef OPARA_BIAS_LATE
-  const int ch = mt * 128 + lane * 4;
-  float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (a.bias) {
-    if (ch + 0 < a.Cout) bias4.x = __ldg(a.bias + ch + 0);
-    if (ch + 1 < a.Cout) bias4.y = __ldg(a.bias + ch + 1);
-    if (ch + 2 < a.Cout) bias4.z = __ldg(a.bias + ch + 2);
-    if (ch + 3 < a.Cout) bias4.w = __ldg(a.bias + ch + 3);
-  }
-#endif
   const uint32_t tile_s = tc::smem_u32(tile);
   // Each warp owns rows r0 + warp, r0 + warp + 10, ...; two rows at a time
   // have every rank's DSMEM load in flight before the first add (one round
@@ -832,14 +797,6 @@ constexpr size_t kPushMaxBytes = 48 * 1024;
 constexpr size_t kSmemLimit = 232448 - 1024;   // 227 KB opt-in smem per CTA, minus static smem headroom
 inline size_t attr_smem(size_t ring) { return std::min(ring + kPushMaxBytes, kSmemLimit); }
 
-bool push_disabled() {
-  static const bool off = [] {
-    const char* e = std::getenv("OPARA_SPLITK_PUSH");
-    return e && e[0] == '0';
-  }();
-  return off;
-}
-
 opara_status set_smem_attr(const TcVariant& v) {
   static bool done[4][2] = {};
   int idx = v.bn == 32 ? 0 : v.bn == 64 ? 1 : v.bn == 128 ? 2 : 3;
@@ -1005,7 +962,7 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
     while (splits > 1) {
       const int rp = ((v[id].bn + splits - 1) / splits + 3) / 4 * 4;
       const size_t rb = static_cast<size_t>(splits) * 128 * rp * 4;
-      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && !push_disabled() && op.i[26] == 0;
+      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && op.i[26] == 0;
       const size_t sm = v[id].smem + (pu ? rb : 0);
       if (clusters <= max_active_clusters(func, splits, sm, attr_smem(v[id].smem))) break;
       --splits;
@@ -1017,7 +974,7 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   a.rows_per = ((v[id].bn + a.splits - 1) / a.splits + 3) / 4 * 4;
   const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
   a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
-            !push_disabled() && op.i[26] == 0) ? 1 : 0;
+            op.i[26] == 0) ? 1 : 0;
   LaunchCfg c;
   c.func = func;
   c.grid = dim3(ceil_div(a.M, v[id].bn), (a.Cout + 127) / 128, a.splits);

@@ -69,9 +69,7 @@ constexpr int kGatherWarps = 4;
 constexpr int kLoadWarp = 4, kMmaWarp = 5;
 constexpr int kThreads = 192;
 constexpr int kMaxSplits = 8;
-#ifndef OPARA_PUSH_MAX_KB
-#define OPARA_PUSH_MAX_KB 48   // split-K push receive buffer limit (KB of smem beyond the ring)
-#endif
+constexpr int kPushMaxKB = 48;   // split-K push receive buffer limit (KB of smem beyond the ring)
 constexpr uint32_t kWBytes = 128 * kBK * 2;  // 8 KB
 
 // Ring depth per tile width.  The 16-wide tile keeps a 24-deep ring (216 KB):
@@ -147,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   constexpr uint32_t kIdesc = tc::instr_desc(1, 128, BN);
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
   static_assert(BN * 128 * 4 <= kStages * kStage, "epilogue tile must fit in the pipeline smem");
-  static_assert(OPARA_PUSH_MAX_KB * 1024 <= kStages * kStage, "push staging blocks must fit in the pipeline smem");
+  static_assert(kPushMaxKB * 1024 <= kStages * kStage, "push staging blocks must fit in the pipeline smem");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -167,7 +165,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   const int mt = blockIdx.y;
   const int kb0 = blockIdx.z * a.kb_per_split;
   const int nkb = min(a.kblocks, kb0 + a.kb_per_split) - kb0;
-#ifndef OPARA_BIAS_LATE
   // the pull epilogue's bias (lane = 4 channels) is a parameter: fetch it now,
   // before griddepcontrol.wait, so its latency hides under the predecessor
   const int ch = mt * 128 + lane * 4;
@@ -177,7 +174,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     for (int e = 0; e < 4; ++e)
       if (ch + e < a.Cout) bias[e] = __ldg(a.bias + ch + e);
   }
-#endif
   // the push epilogue's owner reduction: thread = output channel
   const float push_bias = ((a.push || a.splits > 1) && a.bias && tid < 128 && mt * 128 + tid < a.Cout) ? __ldg(a.bias + mt * 128 + tid) : 0.f;
 
@@ -186,23 +182,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   uint64_t* rbar = accum + 2;
   float* recv = reinterpret_cast<float*>(smem + kStages * kStage + bf_bar_bytes(kStages));
   const bool push = a.push != 0;
-  // Opt-in (-DOPARA_RING_PULL) pull-mode split-K without DSMEM loads: after one
-  // cluster barrier every rank bulk-copies its staged blocks into the owners'
-  // (now idle) rings.  Measured slower than the DSMEM pull in graphs
-  // (GoogLeNet fp32 0.234 -> 0.246 ms, BERT 0.482 -> 0.485 ms), so off by default.
-  const uint32_t stage_bytes = static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4);
-#ifndef OPARA_RING_PULL
-  const bool ring = false;
-#else
-  const bool ring = !push && !a.ws && a.splits > 1 && 2 * stage_bytes <= kStages * kStage;
-#endif
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], 32 * kGatherWarps + 1);  // gather threads + the weight loader
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(accum, 1);
-    if (push || ring) tc::mbar_init(rbar, 1);
+    if (push) tc::mbar_init(rbar, 1);
     tc::fence_barrier_init();
   }
   constexpr int kTmemWarp = kMmaWarp;   // the MMA warp is idle in every epilogue: it frees TMEM off the critical path
@@ -215,13 +201,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     if (tid == 0) {
       // every rank bulk-copies one whole [128][rows_per] block to each owner
       const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
-      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(a.splits * a.rows_per * 128 * 4));
+      // every other rank's block; the owner's own partial stays in its ring
+      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((a.splits - 1) * a.rows_per * 128 * 4));
     }
   } else {
-    if (ring && tid == 0) {   // owners expect every rank's block (the epilogue's cluster barrier orders it)
-      const int r0 = static_cast<int>(tc::cluster_ctarank()) * a.rows_per;
-      if (r0 < BN) tc::mbar_arrive_expect_tx(rbar, stage_bytes);
-    }
     __syncthreads();
   }
   tc::tc_fence_after();
@@ -612,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
     trace_end(trace);
     return;
   }
-  if (push || ring) {
+  if (push) {
     // TMEM -> registers -> this CTA's smem (the drained ring), laid out as one
     // contiguous [128 channels][rows_per] block per owning rank; then one
     // thread bulk-copies each block into its owner's receive slot (TMA engine,
@@ -641,20 +624,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       if (tid == 0) PHASE(8);
     }
     tc::tc_fence_before();
-    // push: the owners' receive buffers sit behind their rings (always free);
-    // ring: they are the owners' rings past the staged blocks, free once every
-    // rank has drained its accumulator, i.e. after one cluster barrier
-    float* rbuf = push ? recv : reinterpret_cast<float*>(smem + stage_bytes);
-    if (ring)
-      tc::cluster_sync();
-    else
-      __syncthreads();
+    // the owners' receive buffers sit behind their rings (always free)
+    float* rbuf = recv;
+    __syncthreads();
     if (tid == 0) {
       PHASE(9);
       const uint32_t block = static_cast<uint32_t>(128 * rp * 4);
       const uint32_t rbar_s = tc::smem_u32(rbar), recv_s = tc::smem_u32(rbuf), stage_s = tc::smem_u32(stage);
       for (int o = 0; o < a.splits && o * rp < BN; ++o)
-        tc::bulk_s2cluster(tc::map_cluster(recv_s + me * block, o), stage_s + o * block, block,
+        if (o != static_cast<int>(me))
+          tc::bulk_s2cluster(tc::map_cluster(recv_s + me * block, o), stage_s + o * block, block,
                            tc::map_cluster(rbar_s, o));
       tc::bulk_commit();
     }
@@ -677,7 +656,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
           for (int z = 0; z < kMaxSplits; ++z)
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (z < a.splits) part[z][e] = rbuf[(z * rp + c0 + e) * 128 + chl];
+              if (z < a.splits) part[z][e] = z == static_cast<int>(me) ? stage[(r0 + c0 + e) * 128 + chl]
+                                                                      : rbuf[(z * rp + c0 + e) * 128 + chl];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             float acc = part[0][e];
@@ -733,15 +713,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   const int rank = splits > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
   const int rows_per = (BN + splits - 1) / splits;
   const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
-#ifdef OPARA_BIAS_LATE
-  const int ch = mt * 128 + lane * 4;
-  float bias[4] = {0.f, 0.f, 0.f, 0.f};
-  if (a.bias) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (ch + e < a.Cout) bias[e] = __ldg(a.bias + ch + e);
-  }
-#endif
   const uint32_t tile_s = tc::smem_u32(tile);
   TO* out = static_cast<TO*>(a.out);
   // a row per warp iteration, every split's DSMEM load issued before the first add
@@ -841,17 +812,9 @@ const BfVariant* bf_variants() {
   return v;
 }
 
-constexpr size_t kPushMaxBytes = OPARA_PUSH_MAX_KB * 1024;
+constexpr size_t kPushMaxBytes = kPushMaxKB * 1024;
 constexpr size_t kSmemLimit = 232448 - 1024;   // 227 KB opt-in smem per CTA, minus static smem headroom
 inline size_t attr_smem(size_t ring) { return std::min(ring + kPushMaxBytes, kSmemLimit); }
-
-bool push_disabled() {
-  static const bool off = [] {
-    const char* v = std::getenv("OPARA_SPLITK_PUSH");
-    return v && v[0] == '0';
-  }();
-  return off;
-}
 
 opara_status set_attr_once(const void* func, size_t smem) {
   static std::mutex mu;
@@ -1002,7 +965,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
     while (splits > 1) {
       const int rp = ((bn + static_cast<int>(splits) - 1) / static_cast<int>(splits) + 3) / 4 * 4;
       const size_t rb = static_cast<size_t>(splits) * 128 * rp * 4;
-      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && !push_disabled() && op.i[26] == 0;
+      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && op.i[26] == 0;
       const size_t sm = v[id].smem + (pu ? rb : 0);
       if (base <= max_clusters(func, static_cast<int>(splits), sm, attr_smem(v[id].smem))) break;
       --splits;
@@ -1015,7 +978,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   a.rows_per = ((bn + a.splits - 1) / a.splits + 3) / 4 * 4;
   const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
   a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
-            !push_disabled() && op.i[26] == 0) ? 1 : 0;
+            op.i[26] == 0) ? 1 : 0;
   a.glob = (a.splits > 1 && op.i[26] == 2) ? 1 : 0;   // reduction through an L2 workspace
   LaunchCfg c;
   c.func = func;

@@ -179,47 +179,6 @@ opara_status check_plan(const opara_exec& ex, const opara_exec::Plan& p) {
   return OPARA_OK;
 }
 
-// Opt-in (OPARA_XSTREAM_PDL=1): measured neutral on every BASELINE model.
-bool xstream_pdl_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("OPARA_XSTREAM_PDL");
-    return v && v[0] == '1';
-  }();
-  return on;
-}
-
-// Every default kernel -> kernel edge of `g` becomes a programmatic edge from
-// the producer's programmatic port: all executor kernels trigger dependents on
-// entry and execute griddepcontrol.wait before reading a predecessor's output.
-opara_status make_edges_programmatic(cudaGraph_t g) {
-  size_t ne = 0;
-  OPARA_CUDA(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));
-  if (ne == 0) return OPARA_OK;
-  std::vector<cudaGraphNode_t> from(ne), to(ne);
-  std::vector<cudaGraphEdgeData> ed(ne);
-  OPARA_CUDA(cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne));
-  std::vector<cudaGraphNode_t> rf, rt;
-  std::vector<cudaGraphEdgeData> old_ed, new_ed;
-  for (size_t k = 0; k < ne; ++k) {
-    if (ed[k].type != cudaGraphDependencyTypeDefault || ed[k].from_port != 0) continue;
-    cudaGraphNodeType a, b;
-    OPARA_CUDA(cudaGraphNodeGetType(from[k], &a));
-    OPARA_CUDA(cudaGraphNodeGetType(to[k], &b));
-    if (a != cudaGraphNodeTypeKernel || b != cudaGraphNodeTypeKernel) continue;
-    rf.push_back(from[k]);
-    rt.push_back(to[k]);
-    old_ed.push_back(ed[k]);
-    cudaGraphEdgeData e = {};
-    e.from_port = cudaGraphKernelNodePortProgrammatic;
-    e.type = cudaGraphDependencyTypeProgrammatic;
-    new_ed.push_back(e);
-  }
-  if (rf.empty()) return OPARA_OK;
-  OPARA_CUDA(cudaGraphRemoveDependencies_v2(g, rf.data(), rt.data(), old_ed.data(), rf.size()));
-  OPARA_CUDA(cudaGraphAddDependencies_v2(g, rf.data(), rt.data(), new_ed.data(), rf.size()));
-  return OPARA_OK;
-}
-
 opara_status capture(opara_exec& ex, const opara_exec::Plan& p, bool traced, opara_exec::Graph* out) {
   const int64_t n = static_cast<int64_t>(ex.ops.size());
   OPARA_CUDA(cudaSetDevice(ex.device));
@@ -276,18 +235,6 @@ opara_status capture(opara_exec& ex, const opara_exec::Plan& p, bool traced, opa
   {
     cudaGraph_t g = nullptr;
     CAP(cudaStreamEndCapture(origin, &g));
-    if (opara::pdl_enabled() && xstream_pdl_enabled()) {
-      // Same-stream kernel edges are already programmatic (PDL launch
-      // attribute); turn the cross-stream ones (the plan's sync events) into
-      // programmatic edges too, so a consumer on another stream also launches
-      // early and waits in griddepcontrol.wait instead of paying a launch
-      // after its producer completes.
-      st = make_edges_programmatic(g);
-      if (st != OPARA_OK) {
-        cudaGraphDestroy(g);
-        goto abort_capture;
-      }
-    }
     out->graph = g;
     cudaError_t e = cudaGraphInstantiate(&out->exec, g, ex.prio.empty() ? 0 : cudaGraphInstantiateFlagUseNodePriority);
     if (e != cudaSuccess) {

@@ -140,29 +140,16 @@ def pack_conv_weights_tf32x3(wk: np.ndarray, rows: int = 128) -> np.ndarray:
     return np.ascontiguousarray(np.stack([image(hi), image(lo)], axis=2)).reshape(-1)
 
 
-def dag_levels(program: Program, alap: bool | None = None) -> list[int]:
-    """Longest-path depth of every op (ops are emitted in topological order).
-    alap=True: as-late-as-possible levels instead (depth minus the longest
-    path to a sink), which puts a short branch beside the tail of the long
-    branches it actually runs next to; OPARA_LEVELS=alap selects it."""
-    if alap is None:
-        alap = os.environ.get("OPARA_LEVELS", "") == "alap"
+def dag_levels(program: Program) -> list[int]:
+    """Longest-path depth of every op (ops are emitted in topological order)."""
     n = len(program.ops)
     preds = [[] for _ in range(n)]
-    succs = [[] for _ in range(n)]
     for u, v in program.edges:
         preds[v].append(u)
-        succs[u].append(v)
     level = [0] * n
     for v in range(n):
         level[v] = 1 + max((level[u] for u in preds[v]), default=-1)
-    if not alap:
-        return level
-    tail = [0] * n                      # longest path (in ops) from v to a sink
-    for v in range(n - 1, -1, -1):
-        tail[v] = 1 + max((tail[w] for w in succs[v]), default=-1)
-    depth = max(level[v] + tail[v] for v in range(n)) if n else 0
-    return [depth - tail[v] for v in range(n)]
+    return level
 
 
 def concurrent_convs(program: Program) -> dict[int, int]:
@@ -204,8 +191,8 @@ def concurrency_targets(program: Program, num_sms: int = 148, scale: float = 1.0
     full-GPU grid: there is nothing to co-reside with."""
     level = dag_levels(program)
     serial = serial_ops(program)
-    weight = _path_weights(program) if os.environ.get("OPARA_SHARES", "") == "slack" else None
-    w = (lambda v: program.ops[v].flops * weight[v]) if weight else (lambda v: program.ops[v].flops)
+    def w(v):
+        return program.ops[v].flops
     work: dict[int, float] = {}
     for v, op in enumerate(program.ops):
         if op.kind == CONV2D:
@@ -215,27 +202,6 @@ def concurrency_targets(program: Program, num_sms: int = 148, scale: float = 1.0
         if op.kind == CONV2D and work.get(level[v]) and v not in serial:
             out[v] = max(8, int(round(scale * num_sms * w(v) / work[level[v]])))
     return out
-
-
-def _path_weights(program: Program) -> list[float]:
-    """(longest estimated-latency path through op v / critical path)^2: ops
-    with slack get smaller SM shares than the critical chain beside them
-    (OPARA_SHARES=slack).  Latency model: 2 us + FLOPs at 50 TFLOP/s."""
-    n = len(program.ops)
-    cost = [2.0 + (op.flops / 50e6 if op.kind == CONV2D else 0.0) for op in program.ops]
-    preds = [[] for _ in range(n)]
-    succs = [[] for _ in range(n)]
-    for u, v in program.edges:
-        preds[v].append(u)
-        succs[u].append(v)
-    head = [0.0] * n
-    for v in range(n):
-        head[v] = cost[v] + max((head[u] for u in preds[v]), default=0.0)
-    tail = [0.0] * n
-    for v in range(n - 1, -1, -1):
-        tail[v] = cost[v] + max((tail[x] for x in succs[v]), default=0.0)
-    cp = max(head) if n else 1.0
-    return [((head[v] + tail[v] - cost[v]) / cp) ** 2 for v in range(n)]
 
 
 SPLITK_MODES = {"push": 0, "pull": 1, "global": 2}
@@ -423,7 +389,7 @@ class ScheduledGraph:
         self.schedule = make_order(self.graph, policy, self.gpu_config, seed)
         self.seq_plan = single_stream_plan(self.graph)
         self.seq_schedule = LaunchSchedule(tuple(self.graph.topo_sort()), "sequential")
-        if priorities if priorities is not None else os.environ.get("OPARA_PRIORITY") == "1":
+        if priorities:
             self.set_priorities(self.critical_priorities())
         self.capture(SLOT_PARALLEL, self.plan, self.schedule)
         self.capture(SLOT_SEQUENTIAL, self.seq_plan, self.seq_schedule)

@@ -378,6 +378,21 @@ class _Lowerer:
         if x.dtype != "f32":
             raise LoweringError(f"{node.name}: the SIMT linear head expects fp32 rows")
         out = self.new_tensor((m, nout), dtype="f32")
+        if m > 1 and k % 4 == 0:
+            # a real GEMM (several rows, e.g. a DeepFM request batch): a 1x1 conv over
+            # [rows, 1, 1, features], so it runs on the fp32 tensor-core engine (3xTF32
+            # tcgen05) or the exact-FFMA SIMT conv, whichever the per-shape tuner measures
+            # faster.  Single-row GEMVs stay on the bandwidth-bound SIMT linear kernel.
+            wk = lin.weight.detach().double().cpu().numpy().T.astype(np.float32).copy()
+            bias = (lin.bias.detach().float().cpu().numpy() if lin.bias is not None
+                    else np.zeros(nout, dtype=np.float32))
+            self.emit(LoweredOp(CONV2D, "gemm", OpClass.COMPUTE,
+                                dict(N=m, H=1, W=1, Cin=k, OH=1, OW=1, Cout=nout, R=1, S=1, sh=1, sw=1, ph=0,
+                                     pw=0, relu=act, relu_in=0),
+                                [x], out, wk, bias, flops=2 * m * k * nout,
+                                bytes_min=4 * (m * k + wk.size + bias.size + m * nout), label=node.name))
+            self.env[tail] = out
+            return
         wt = lin.weight.detach().float().cpu().contiguous().numpy()
         b = lin.bias.detach().float().cpu().numpy() if lin.bias is not None else None
         op = LoweredOp(LINEAR, "gemm", OpClass.COMPUTE, dict(M=m, K=k, N=nout, act=act), [x], out,

@@ -186,6 +186,28 @@ def measure_orders(sg, orders, iters: int = 200, warmup: int = 20, flush_l2: boo
     return out
 
 
+def critical_path_first_order(g: ComputationGraph, cost: dict[int, float]) -> tuple[int, ...]:
+    """Diagnostic baseline (not a reference policy): list scheduling that
+    always launches the ready op with the longest remaining path (its own
+    cost plus the longest cost path to a sink), ties by ascending id."""
+    import heapq
+    tail: dict[int, float] = {}
+    for v in reversed(g.topo_sort()):
+        tail[v] = cost[v] + max((tail[w] for w in g.successors(v)), default=0.0)
+    missing = {v: len(g.predecessors(v)) for v in g.node_ids}
+    ready = [(-tail[v], v) for v in g.node_ids if missing[v] == 0]
+    heapq.heapify(ready)
+    out = []
+    while ready:
+        _, v = heapq.heappop(ready)
+        out.append(v)
+        for w in g.successors(v):
+            missing[w] -= 1
+            if missing[w] == 0:
+                heapq.heappush(ready, (-tail[w], w))
+    return tuple(out)
+
+
 def search_measured(sg, limit: int = 5000, iters: int = 200, recheck: int = 8, rounds: int = 3) -> dict:
     """Rank Alg. 2's order among every linear extension of `sg`'s DAG (up to
     `limit`) by measured latency.  Every order is timed in `rounds` interleaved
@@ -204,6 +226,8 @@ def search_measured(sg, limit: int = 5000, iters: int = 200, recheck: int = 8, r
     lat = np.median(np.asarray(passes), axis=0)
     named = {pol: tuple(make_order(g, pol, sg.gpu_config).order) for pol in ("opara", "dfs", "wavefront",
                                                                               "sequential")}
+    named["critical_path_first"] = critical_path_first_order(
+        g, {v: sg.profile[v - 1]["isolated_us"] for v in g.node_ids})
     top = [orders[i] for i in np.argsort(lat)[:recheck]]
     final_set = list(dict.fromkeys(top + list(named.values())))
     fin = np.median(np.asarray([measure_orders(sg, final_set, iters=iters * 2) for _ in range(rounds)]), axis=0)
@@ -221,7 +245,9 @@ def search_measured(sg, limit: int = 5000, iters: int = 200, recheck: int = 8, r
         "latency_ms": {"min": float(sorted_lat[0]), "median": float(np.median(lat)),
                        "max": float(sorted_lat[-1])},
         "best_order": list(min(fin_of, key=fin_of.get)), "best_ms": float(min(fin_of.values())),
-        "policies": {pol: {"ms": fin_of[o], "rank": rank(o), "percentile": (rank(o) or 0) / len(orders)}
-                     for pol, o in named.items()},
+        "policies": {pol: {"ms": fin_of[o], "rank": rank(o), "percentile": (rank(o) or 0) / len(orders),
+                           "order": list(o)} for pol, o in named.items()},
+        "isolated_us": {v: sg.profile[v - 1]["isolated_us"] for v in g.node_ids},
+        "classes": {v: g.node(v).op_class.value for v in g.node_ids},
         "iters": iters, "rounds": rounds,
     }

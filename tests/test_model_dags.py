@@ -133,19 +133,6 @@ def test_serial_ops_keep_full_grids():
     assert 0 in engine.serial_ops(g) and 1 in engine.serial_ops(g)   # PACK_INPUT -> stem conv
 
 
-def test_alap_levels_and_slack_weights():
-    """Opt-in share policies: ALAP levels never precede ASAP ones and agree on
-    serial ops; slack weights are in (0, 1] with the critical chain at 1."""
-    model, x = zoo.build("inception_v3")
-    prog = frontend.lower(model, x)
-    asap, alap = engine.dag_levels(prog, alap=False), engine.dag_levels(prog, alap=True)
-    assert all(b >= a for a, b in zip(asap, alap))
-    assert all(asap[v] == alap[v] for v in engine.serial_ops(prog))
-    w = engine._path_weights(prog)
-    assert all(0 < x <= 1 + 1e-12 for x in w) and max(w) == pytest.approx(1.0)
-    assert all(w[v] == pytest.approx(1.0) for v in engine.serial_ops(prog))
-
-
 def _workload(name):
     if name == "bert_base":
         m, _, ids = zoo.build_bert()
