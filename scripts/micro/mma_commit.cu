@@ -21,7 +21,7 @@ __device__ __forceinline__ uint64_t desc64(uint32_t saddr) {
 }
 
 template <int BN>
-__global__ void bench(int iters, int per, int wait_each, long long* out) {
+__global__ void bench(int iters, int per, int wait_each, int mode, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar[64];
@@ -38,7 +38,68 @@ __global__ void bench(int iters, int per, int wait_each, long long* out) {
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tslot;
-  if (threadIdx.x == 0) {
+  if (mode >= 3 && warp == 0) {
+    // warp-uniform issue: every lane runs the loop, descriptors precomputed and
+    // advanced with 64-bit adds, the MMA itself under elect.sync
+    constexpr uint32_t id2 = tc::instr_desc(2, 128, 2 * BN), id1 = tc::instr_desc(2, 128, BN);
+    const uint32_t a = tc::smem_u32(smem), b = a + 32768;
+    const uint64_t da = desc64(a), dl = desc64(a + 16384), db = desc64(b), db2 = desc64(b + 8192);
+    long long t0 = clock64();
+    int c = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll 1
+      for (int m = 0; m < 96; m += 2) {
+        const uint64_t off = (m & 2) ? 2 : 0;
+        if (tc::elect_one()) {
+          if (mode == 3) {
+            tc::mma_tf32(tmem, da + off, db + off, id2, 1);
+            tc::mma_tf32(tmem + 2 * BN, dl + off, db + off, id1, 1);
+          } else {
+            tc::mma_tf32(tmem, da + off, db + off, id1, 1);
+            tc::mma_tf32(tmem + BN, da + off, db2 + off, id1, 1);
+            tc::mma_tf32(tmem + 2 * BN, dl + off, db + off, id1, 1);
+          }
+        }
+        __syncwarp();
+        if ((m + 2) % per == 0) {
+          if (tc::elect_one()) tc::mma_commit(&bar[c % 64]);
+          __syncwarp();
+          ++c;
+        }
+      }
+    }
+    if (tc::elect_one()) tc::mma_commit(&bar[c % 64]);
+    __syncwarp();
+    tc::mbar_wait(&bar[c % 64], (c / 64) & 1);
+    long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = t1 - t0;
+  } else if (mode == 5 && threadIdx.x == 0) {
+    // single issuing thread, descriptors = loop-invariant bases + compile-time
+    // offsets (the stage loop unrolled by the ring depth, as in the conv)
+    constexpr uint32_t id2 = tc::instr_desc(2, 128, 2 * BN), id1 = tc::instr_desc(2, 128, BN);
+    const uint32_t a = tc::smem_u32(smem);
+    const uint64_t d0 = desc64(a);
+    long long t0 = clock64();
+    int c = 0;
+    for (int it = 0; it < iters; ++it) {
+      for (int m0 = 0; m0 < 96; m0 += 8) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {          // 4 "stages" of one 8-wide k step pair each
+          const uint64_t st = d0 + s * (6144 >> 4);
+#pragma unroll
+          for (int ks = 0; ks < 1; ++ks) {
+            tc::mma_tf32(tmem, st + 2 * ks, st + (32768 >> 4) + 2 * ks, id2, 1);
+            tc::mma_tf32(tmem + 2 * BN, st + (16384 >> 4) + 2 * ks, st + (32768 >> 4) + 2 * ks, id1, 1);
+          }
+          if (per <= 4) { tc::mma_commit(&bar[c % 64]); ++c; }
+        }
+      }
+    }
+    tc::mma_commit(&bar[c % 64]);
+    tc::mbar_wait(&bar[c % 64], (c / 64) & 1);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = t1 - t0;
+  } else if (mode < 3 && threadIdx.x == 0) {
     constexpr uint32_t id2 = tc::instr_desc(2, 128, 2 * BN), id1 = tc::instr_desc(2, 128, BN);
     const uint32_t a = tc::smem_u32(smem), b = a + 32768;
     long long t0 = clock64();
@@ -46,8 +107,17 @@ __global__ void bench(int iters, int per, int wait_each, long long* out) {
     for (int it = 0; it < iters; ++it) {
       for (int m = 0; m < 96; m += 2) {
         const uint64_t off = (m & 2) ? 2 : 0;     // next 32-byte k slice of the atom
-        tc::mma_tf32(tmem, desc64(a) + off, desc64(b) + off, id2, 1);
-        tc::mma_tf32(tmem + 2 * BN, desc64(a + 16384) + off, desc64(b) + off, id1, 1);
+        if (mode == 0) {          // the conv: hi x [hi; lo] (N = 2 BN), lo x hi (N = BN)
+          tc::mma_tf32(tmem, desc64(a) + off, desc64(b) + off, id2, 1);
+          tc::mma_tf32(tmem + 2 * BN, desc64(a + 16384) + off, desc64(b) + off, id1, 1);
+        } else if (mode == 1) {   // same shape twice: lo x [hi; hi'] (N = 2 BN, half wasted)
+          tc::mma_tf32(tmem, desc64(a) + off, desc64(b) + off, id2, 1);
+          tc::mma_tf32(tmem + 2 * BN, desc64(a + 16384) + off, desc64(b) + off, id2, 1);
+        } else {                  // three N = BN MMAs (hh, hl, lh), one shape
+          tc::mma_tf32(tmem, desc64(a) + off, desc64(b) + off, id1, 1);
+          tc::mma_tf32(tmem + BN, desc64(a) + off, desc64(b + 8192) + off, id1, 1);
+          tc::mma_tf32(tmem + 2 * BN, desc64(a + 16384) + off, desc64(b) + off, id1, 1);
+        }
         if ((m + 2) % per == 0) {
           tc::mma_commit(&bar[c % 64]);
           if (wait_each) tc::mbar_wait(&bar[c % 64], (c / 64) & 1);
@@ -66,25 +136,28 @@ __global__ void bench(int iters, int per, int wait_each, long long* out) {
 }
 
 template <int BN>
-void run(long long* d, int per, int wait_each) {
+void run(long long* d, int per, int wait_each, int mode, int smem_kb = 100) {
   auto f = bench<BN>;
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kb * 1024);
   const int iters = 20;
   long long h = 0;
   for (int rep = 0; rep < 3; ++rep) {
-    f<<<148, 128, 100 * 1024>>>(iters, per, wait_each, d);
+    f<<<148, 128, smem_kb * 1024>>>(iters, per, wait_each, mode, d);
     cudaDeviceSynchronize();
   }
   cudaError_t e = cudaGetLastError();
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  printf("BN=%3d commit every %2d MMAs, %s: %6.1f cyc per (N=2BN, N=BN) pair  %s\n", BN, per,
-         wait_each ? "wait each commit" : "no wait        ", h / (iters * 48.0), cudaGetErrorString(e));
+  printf("smem %3d KB mode %d (%s) BN=%3d commit every %2d pairs, %s: %6.1f cyc per 8-wide k step  %s\n", smem_kb, mode,
+         mode == 0 ? "N=2BN + N=BN   " : mode == 1 ? "N=2BN + N=2BN  " : mode == 2 ? "3 x N=BN       " :
+         mode == 3 ? "warp N=2BN+N=BN" : mode == 4 ? "warp 3 x N=BN  " : "unrolled consts", BN, per / 2,
+         wait_each ? "wait each" : "no wait  ", h / (iters * 48.0), cudaGetErrorString(e));
 }
 
 int main() {
   long long* d;
   cudaMalloc(&d, 64);
-  for (int per : {2, 4, 8, 96})
-    for (int w : {0, 1}) { run<32>(d, per, w); run<64>(d, per, w); }
+  for (int kb : {140})
+    for (int mode : {0, 5})
+      for (int per : {4, 96}) { run<32>(d, per, 0, mode, kb); run<64>(d, per, 0, mode, kb); }
   return 0;
 }
