@@ -472,17 +472,31 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   const int rows_per = (BN + splits - 1) / splits;
   const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
   const uint32_t tile_s = tc::smem_u32(tile);
-  // Each warp owns rows r0 + warp, r0 + warp + 10, ...; two rows at a time
-  // have every rank's DSMEM load in flight before the first add (one round
-  // trip per row pair instead of per row), summed in rank order.
-  constexpr int kWarps = kThreads / 32;
-  auto finish = [&](int row, float4 acc) {
+  for (int row = r0 + warp; row < r1; row += kThreads / 32) {
+    const int p = n0 + row;
+    if (p >= a.M) break;
+    const uint32_t off = static_cast<uint32_t>((row * 128 + lane * 4) * 4);
+    float4 acc;
+    if (splits > 1) {
+      float4 part[kMaxSplits];
+#pragma unroll
+      for (int z = 0; z < kMaxSplits; ++z)
+        if (z < splits) part[z] = tc::ld_dsmem_f4(tc::map_cluster(tile_s + off, z));
+      acc = part[0];
+#pragma unroll
+      for (int z = 1; z < kMaxSplits; ++z)
+        if (z < splits) {
+          acc.x += part[z].x; acc.y += part[z].y; acc.z += part[z].z; acc.w += part[z].w;
+        }
+    } else {
+      acc = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(tile) + off);
+    }
     acc.x += bias4.x; acc.y += bias4.y; acc.z += bias4.z; acc.w += bias4.w;
     if (a.relu) {
       acc.x = apply_act(acc.x, a.relu); acc.y = apply_act(acc.y, a.relu);
       acc.z = apply_act(acc.z, a.relu); acc.w = apply_act(acc.w, a.relu);
     }
-    float* dst = a.out + static_cast<int64_t>(n0 + row) * a.out_cs + a.out_coff + ch;
+    float* dst = a.out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
     if (a.vec_out && ch + 3 < a.Cout) {
       *reinterpret_cast<float4*>(dst) = acc;
     } else {
@@ -490,34 +504,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       if (ch + 1 < a.Cout) dst[1] = acc.y;
       if (ch + 2 < a.Cout) dst[2] = acc.z;
       if (ch + 3 < a.Cout) dst[3] = acc.w;
-    }
-  };
-  const int r_end = min(r1, a.M - n0);
-  for (int row = r0 + warp; row < r_end; row += 2 * kWarps) {
-    const int row2 = row + kWarps;
-    const bool two = row2 < r_end;
-    const uint32_t off = static_cast<uint32_t>((row * 128 + lane * 4) * 4);
-    const uint32_t off2 = static_cast<uint32_t>((row2 * 128 + lane * 4) * 4);
-    if (splits > 1) {
-      float4 part[kMaxSplits], part2[kMaxSplits];
-#pragma unroll
-      for (int z = 0; z < kMaxSplits; ++z)
-        if (z < splits) {
-          part[z] = tc::ld_dsmem_f4(tc::map_cluster(tile_s + off, z));
-          if (two) part2[z] = tc::ld_dsmem_f4(tc::map_cluster(tile_s + off2, z));
-        }
-      float4 acc = part[0], acc2 = part2[0];
-#pragma unroll
-      for (int z = 1; z < kMaxSplits; ++z)
-        if (z < splits) {
-          acc.x += part[z].x; acc.y += part[z].y; acc.z += part[z].z; acc.w += part[z].w;
-          acc2.x += part2[z].x; acc2.y += part2[z].y; acc2.z += part2[z].z; acc2.w += part2[z].w;
-        }
-      finish(row, acc);
-      if (two) finish(row2, acc2);
-    } else {
-      finish(row, *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(tile) + off));
-      if (two) finish(row2, *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(tile) + off2));
     }
   }
   DBG(6);
