@@ -32,6 +32,7 @@
 #include "ops.h"
 #include "status.h"
 #include "tc_common.cuh"
+#include "tma_host.h"
 
 #include <cstdlib>
 #include <map>
@@ -55,6 +56,7 @@ constexpr uint32_t kWBytes = 128 * kBKF * 4;  // one precision plane of the W st
 __host__ __device__ constexpr int tc_stages(int bn) { return bn == 32 ? 5 : bn == 64 ? 4 : bn == 128 ? 6 : 4; }
 
 struct TcArgs {
+  CUtensorMap tmap;                 // im2col map of the input view (kLoad == kLoadTma only)
   const float* __restrict__ in;
   const float* __restrict__ wpack;  // [m_tiles][kblocks][hi|lo][chunk][rg][8][4]
   const float* __restrict__ bias;
@@ -99,8 +101,13 @@ __device__ __forceinline__ void drain_accumulators(uint32_t trow, int half, Put 
   }
 }
 
-template <int BN, bool kVec>
-__global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsigned long long* trace) {
+// Activation load path: scalar 4-byte cp.async gathers, 16-byte cp.async
+// gathers (4 channels), or TMA im2col loads of the whole stage (one thread).
+enum { kLoadScalar = 0, kLoadVec = 1, kLoadTma = 2 };
+
+template <int BN, int kLoad>
+__global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(const __grid_constant__ TcArgs a, unsigned long long* trace) {
+  constexpr bool kVec = kLoad == kLoadVec;
   constexpr int kStages = tc_stages(BN);
   constexpr uint32_t kXBytes = BN * kBKF * 4;
   constexpr uint32_t kStage = 2 * kWBytes + 2 * kXBytes;
@@ -165,7 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], 32 * (kProducerWarps / 2) + 1);  // converters + the weight loader
-      tc::mbar_init(&landed[s], 32 * (kProducerWarps / 2));   // one noinc arrive per gather thread
+      // one noinc arrive per gather thread, or the TMA thread's expect_tx arrive
+      tc::mbar_init(&landed[s], kLoad == kLoadTma ? 1 : 32 * (kProducerWarps / 2));
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(accum, 1);
@@ -203,7 +211,34 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(TcArgs a, unsign
       return static_cast<uint32_t>(rw + 4 * j) * kSbo + r8 * 64u +
              static_cast<uint32_t>((cl ^ ((r8 >> 1) & 3)) * 16);
     };
-    if (gather) {
+    if (kLoad == kLoadTma && gather) {
+      // One lane streams each stage's X tile (BN pixels x 16 channels of one
+      // tap, K = (r*S + s)*Cin + c with Cin % 16 == 0) into the hi plane with
+      // a TMA im2col load; padding and the tile tail arrive as zeros.
+      if (warp == 0 && lane == 0) {
+        const int ohw = a.OH * a.OW;
+        const int b = n0 / ohw, rem = n0 - b * ohw, oh = rem / a.OW, ow = rem - oh * a.OW;
+        const int w0 = ow * a.sw - a.pw, h0 = oh * a.sh - a.ph;
+        const int kc = kb0 * kBKF, rs = kc / a.Cin;
+        int dc = kc - rs * a.Cin, dr = rs / a.S, dq = rs - dr * a.S;
+        pdl_wait();
+        trace_begin(trace);
+        for (int i = 0; i < nkb; ++i) {
+          const int s = i % kStages;
+          if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+          tc::mbar_arrive_expect_tx(&landed[s], kXBytes);
+          tc::tma_im2col_4d(smem + s * kStage + 2 * kWBytes, &a.tmap, dc, w0, h0, b, dq, dr, &landed[s]);
+          dc += kBKF;
+          if (dc == a.Cin) {
+            dc = 0;
+            if (++dq == a.S) {
+              dq = 0;
+              ++dr;
+            }
+          }
+        }
+      }
+    } else if (gather) {
       int pb[kRowsPerThread], pih[kRowsPerThread], piw[kRowsPerThread];
       const int ohw = a.OH * a.OW;
 #pragma unroll
@@ -761,15 +796,16 @@ constexpr size_t tc_smem_bytes() {
 
 struct TcVariant {
   int bn;
-  const void* func[2];
+  const void* func[3];   // [kLoad]
   size_t smem;
 };
 
 template <int BN>
 TcVariant make_tc() {
   return {BN,
-          {reinterpret_cast<const void*>(&conv2d_tc_tf32x3<BN, false>),
-           reinterpret_cast<const void*>(&conv2d_tc_tf32x3<BN, true>)},
+          {reinterpret_cast<const void*>(&conv2d_tc_tf32x3<BN, kLoadScalar>),
+           reinterpret_cast<const void*>(&conv2d_tc_tf32x3<BN, kLoadVec>),
+           reinterpret_cast<const void*>(&conv2d_tc_tf32x3<BN, kLoadTma>)},
           tc_smem_bytes<BN>()};
 }
 
@@ -784,9 +820,9 @@ constexpr size_t kSmemLimit = 232448 - 1024;   // 227 KB opt-in smem per CTA, mi
 inline size_t attr_smem(size_t ring) { return std::min(ring + kPushMaxBytes, kSmemLimit); }
 
 opara_status set_smem_attr(const TcVariant& v) {
-  static bool done[4][2] = {};
+  static bool done[4][3] = {};
   int idx = v.bn == 32 ? 0 : v.bn == 64 ? 1 : v.bn == 128 ? 2 : 3;
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     if (done[idx][k]) continue;
     cudaError_t e = cudaFuncSetAttribute(v.func[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(attr_smem(v.smem)));
@@ -940,7 +976,10 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   const int64_t target = op.i[21] > 0 ? op.i[21] : 148;
   choose_tiling(a, target, (op.variant >= 0 && op.variant < count) ? op.variant : -1,
                 op.i[19] > 1 ? static_cast<int>(op.i[19]) : op.i[19] == -1 ? 1 : 0, &id, &splits);
-  const void* func = v[id].func[vec ? 1 : 0];
+  // TMA im2col loads whenever the view allows them (16-channel taps, 16-byte
+  // aligned view); the pixel tile of this variant is the map's pixel count
+  const bool tma = !nchw && im2col_eligible(a.in, 4, a.Cin, in_cs, a.in_coff, a.H, a.W, a.OH, a.OW, a.sh, a.sw, a.ph, a.pw, kBKF);
+  const void* func = v[id].func[tma ? kLoadTma : vec ? kLoadVec : kLoadScalar];
   if (splits > 1 && op.i[19] <= 1) {
     // clusters must be co-resident inside a GPC: keep every cluster in the
     // first wave (a second wave doubles the latency of the whole conv)
@@ -970,6 +1009,9 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   if (dry) return OPARA_OK;
   opara_status st = set_smem_attr(v[id]);
   if (st != OPARA_OK) return st;
+  if (tma && !make_im2col_map(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, op.p[0], a.N, a.H, a.W, a.Cin, in_cs,
+                              a.in_coff, a.OH, a.OW, a.sh, a.sw, a.ph, a.pw, kBKF, v[id].bn))
+    return fail(OPARA_ERR_CUDA, "conv2d_tc: cuTensorMapEncodeIm2col failed");
   void* args[] = {&a, &trace};
   return launch_kernel(c, args, s, a.splits > 1 ? static_cast<unsigned>(a.splits) : 1u);
 }

@@ -29,6 +29,7 @@
 #include "ops.h"
 #include "status.h"
 #include "tc_common.cuh"
+#include "tma_host.h"
 
 namespace opara {
 namespace {
@@ -84,8 +85,10 @@ __host__ __device__ constexpr int bf_bar_bytes(int stages) { return ((2 * stages
 // 16-byte smem chunk assembled from 8- / 4-byte cp.asyncs of 4 / 2 channels
 // (Cin % 4 / % 2 == 0, e.g. NASNet's 84 / 42 channels), every sub-chunk with
 // its own incrementally tracked (r, s, c); scalar register paths otherwise.
-enum GatherMode { kVecBf16 = 0, kScalarBf16 = 1, kScalarF32 = 2, kSub4 = 3, kSub2 = 4 };
-constexpr int kModes = 5;
+// kTma: one thread loads each stage's X tile with a TMA im2col load (bf16
+// input, Cin % 32 == 0, 16-byte aligned view, no fused input ReLU).
+enum GatherMode { kVecBf16 = 0, kScalarBf16 = 1, kScalarF32 = 2, kSub4 = 3, kSub2 = 4, kTma = 5 };
+constexpr int kModes = 6;
 
 __device__ __forceinline__ void cp_async_sub(uint32_t dst, const void* src, int bytes, bool ok) {
   if (bytes == 8)
@@ -95,6 +98,7 @@ __device__ __forceinline__ void cp_async_sub(uint32_t dst, const void* src, int 
 }
 
 struct BfArgs {
+  CUtensorMap tmap;                         // im2col map of the input view (kTma only)
   const void* in;
   const __nv_bfloat16* __restrict__ wpack;  // [m_tiles][kblocks][atom][row][chunk][8]
   const float* __restrict__ bias;
@@ -135,7 +139,7 @@ __device__ __forceinline__ float act_fn(float v, int act) {
 }
 
 template <int BN, int kMode, typename TO>
-__global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned long long* trace) {
+__global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_constant__ BfArgs a, unsigned long long* trace) {
   constexpr int kStages = bf_stages(BN);
   constexpr uint32_t kXBytes = BN * kBK * 2;
   constexpr uint32_t kStage = kWBytes + kXBytes;
@@ -184,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
   const bool push = a.push != 0;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      tc::mbar_init(&full[s], 32 * kGatherWarps + 1);  // gather threads + the weight loader
+      // gather threads (or the TMA thread's expect_tx arrive) + the weight loader
+      tc::mbar_init(&full[s], kMode == kTma ? 2 : 32 * kGatherWarps + 1);
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(accum, 1);
@@ -256,7 +261,31 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(BfArgs a, unsigned
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&full[st]);
     };
-    if constexpr (kMode == kVecBf16) {
+    if constexpr (kMode == kTma) {
+      // k = (r*S + s)*Cin + c with Cin % 32 == 0: every stage is one tap's
+      // 32-channel slice of BN output pixels; padding and the tile tail are zeros
+      if (tid == 0) {
+        const int ohw = a.OH * a.OW;
+        const int b = n0 / ohw, rem = n0 - b * ohw, oh = rem / a.OW, ow = rem - oh * a.OW;
+        const int w0 = ow * a.sw - a.pw, h0 = oh * a.sh - a.ph;
+        const int kc = kb0 * kBK, rs = kc / a.Cin;
+        int dc = kc - rs * a.Cin, dr = rs / a.S, dq = rs - dr * a.S;
+        for (int i = 0; i < nkb; ++i) {
+          const int s = i % kStages;
+          if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+          tc::mbar_arrive_expect_tx(&full[s], kXBytes);
+          tc::tma_im2col_4d(smem + s * kStage + kWBytes, &a.tmap, dc, w0, h0, b, dq, dr, &full[s]);
+          dc += kBK;
+          if (dc == a.Cin) {
+            dc = 0;
+            if (++dq == a.S) {
+              dq = 0;
+              ++dr;
+            }
+          }
+        }
+      }
+    } else if constexpr (kMode == kVecBf16) {
       const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(a.in);
       const __nv_bfloat16* rowbase[kRowsPerThread];
 #pragma unroll
@@ -803,6 +832,8 @@ BfVariant make_bf() {
   v.func[kSub4][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kSub4, float>);
   v.func[kSub2][0] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kSub2, __nv_bfloat16>);
   v.func[kSub2][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kSub2, float>);
+  v.func[kTma][0] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kTma, __nv_bfloat16>);
+  v.func[kTma][1] = reinterpret_cast<const void*>(&conv2d_tc_bf16<BN, kTma, float>);
   v.smem = bf_smem_bytes<BN>();
   return v;
 }
@@ -902,7 +933,13 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
     return !nchw && a.Cin % g == 0 && in_cs % g == 0 && a.in_coff % g == 0 &&
            reinterpret_cast<uintptr_t>(a.in) % (2 * g) == 0;
   };
-  const int mode = in_f32 ? kScalarF32 : vec_ok(8) ? kVecBf16 : vec_ok(4) ? kSub4 : vec_ok(2) ? kSub2 : kScalarBf16;
+  const bool tma = !in_f32 && !nchw && !a.relu_in &&
+                   im2col_eligible(a.in, 2, a.Cin, in_cs, a.in_coff, a.H, a.W, a.OH, a.OW, a.sh, a.sw, a.ph, a.pw, kBK);
+  const int mode = in_f32 ? kScalarF32 : tma ? kTma : vec_ok(8) ? kVecBf16 : vec_ok(4) ? kSub4 : vec_ok(2) ? kSub2 : kScalarBf16;
+  auto encode = [&](int bn) {
+    return !tma || make_im2col_map(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, op.p[0], a.N, a.H, a.W, a.Cin, in_cs,
+                                   a.in_coff, a.OH, a.OW, a.sh, a.sw, a.ph, a.pw, kBK, bn);
+  };
   const int align = out_f32 ? 16 : 8;
   a.vec_out = (a.out_cs % 4 == 0 && a.out_coff % 4 == 0 && reinterpret_cast<uintptr_t>(a.out) % align == 0) ? 1 : 0;
   const BfVariant* v = bf_variants();
@@ -937,6 +974,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
     if (dry) return OPARA_OK;
     opara_status st = set_attr_once(c.func, attr_smem(v[lid].smem));
     if (st != OPARA_OK) return st;
+    if (!encode(v[lid].bn)) return fail(OPARA_ERR_CUDA, "conv2d_tc_bf16: cuTensorMapEncodeIm2col failed");
     void* args[] = {&a, &trace};
     return launch_kernel_cluster(c, args, s, dim3(1, static_cast<unsigned>(mtiles), 1));
   }
@@ -1000,6 +1038,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   }
   opara_status st = set_attr_once(func, attr_smem(v[id].smem));
   if (st != OPARA_OK) return st;
+  if (!encode(bn)) return fail(OPARA_ERR_CUDA, "conv2d_tc_bf16: cuTensorMapEncodeIm2col failed");
   void* args[] = {&a, &trace};
   return launch_kernel(c, args, s, (a.splits > 1 && !a.glob) ? static_cast<unsigned>(a.splits) : 1u);
 }

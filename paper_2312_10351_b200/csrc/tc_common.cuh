@@ -83,6 +83,20 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint64_t bytes
   }
 }
 
+// TMA im2col load (tensor map from tma_host.h, a __grid_constant__ kernel
+// parameter): channels [c, c + cpp) of pixelsPerColumn consecutive output
+// pixels starting at window origin (w, h, n), tap offset (s, r), into `dst`
+// in the map's swizzle; completion counted in bytes on `bar`.
+__device__ __forceinline__ void tma_im2col_4d(void* dst, const void* tmap, int c, int w, int h, int n, int s, int r,
+                                              uint64_t* bar) {
+  const uint16_t os = static_cast<uint16_t>(s), orr = static_cast<uint16_t>(r);
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(bar)), "h"(os), "h"(orr)
+      : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05
 
 // Allocate `ncols` TMEM columns (power of two >= 32); one full warp calls it.

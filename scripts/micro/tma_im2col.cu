@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <vector>
+#include <cstdlib>
 
 __global__ void k_load(const __grid_constant__ CUtensorMap map, int* out, int c, int w, int h, int n, int offw, int offh, int bytes) {
   extern __shared__ __align__(1024) int sm[];
@@ -29,7 +30,7 @@ __global__ void k_load(const __grid_constant__ CUtensorMap map, int* out, int c,
   for (int i = threadIdx.x; i < bytes / 4; i += blockDim.x) out[i] = sm[i];
 }
 
-int main() {
+int main(int argc, char** argv) {
   struct Case { const char* name; int N, H, W, C, lw, lh, uw, uh, cpp, ppc, sw, sh, c, w, h, n, offw, offh; };
   // lower/upper corners given as {W, H} (array index 0 = W) -- the probe checks this
   Case cases[] = {
@@ -39,8 +40,15 @@ int main() {
     {"1x7 pw3 ph0 H=W=5 (lw=-3,lh=0,uw=-3,uh=0), start(w=-3,h=0) off(3,0)", 1, 5, 5, 32, -3, 0, -3, 0, 16, 32, 1, 1, 0, -3, 0, 0, 3, 0},
     {"3x3 p0 s2 H=W=7 (OH=3), start(0,0) off(0,0)", 2, 7, 7, 32, 0, 0, -2, -2, 16, 24, 2, 2, 0, 0, 0, 0, 0, 0},
     {"3x3 p0 s2 H=W=7, start(0,0) off(2,2) n wrap", 2, 7, 7, 32, 0, 0, -2, -2, 16, 24, 2, 2, 0, 0, 0, 0, 2, 2},
+    // subsample(x, 1) -> 1x1 stride 2: pad -1, box [1, W] (past the edge), OW = (W+1)/2
+    {"1x1 s2 pad -1 H=W=7 (lower 1, upper 1), start(1,1)", 1, 7, 7, 32, 1, 1, 1, 1, 16, 16, 2, 2, 0, 1, 1, 0, 0, 0},
+    {"1x1 s2 pad -1 H=W=7 (lower 1, upper -1), start(1,1)", 1, 7, 7, 32, 1, 1, -1, -1, 16, 16, 2, 2, 0, 1, 1, 0, 0, 0},
+    {"1x1 s2 pad 0 H=W=7 (lower 0, upper 0), start(0,0)", 1, 7, 7, 32, 0, 0, 0, 0, 16, 16, 2, 2, 0, 0, 0, 0, 0, 0},
   };
+  const int only = argc > 1 ? atoi(argv[1]) : -1;
+  int idx = -1;
   for (auto& cs : cases) {
+    if (only >= 0 && ++idx != only) continue;
     const size_t ne = (size_t)cs.N * cs.H * cs.W * cs.C;
     std::vector<int> hin(ne);
     for (int n = 0; n < cs.N; ++n) for (int h = 0; h < cs.H; ++h) for (int w = 0; w < cs.W; ++w) for (int c = 0; c < cs.C; ++c)

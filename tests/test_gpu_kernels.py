@@ -198,3 +198,76 @@ def test_pool_matches_torch(name, make, c, dtype):
         ref = m.double()(x.double()).float()
     assert y.shape == ref.shape
     assert _rel(y, ref) < (1e-2 if dtype == "bf16" else 1e-5), name
+
+
+TMA_CASES = [
+    # cin, cout, kernel, stride, pad, hw, batch
+    (64, 64, 1, 1, 0, 56, 1),
+    (192, 96, 3, 1, 1, 28, 2),          # image wrap inside a pixel tile
+    (160, 192, (1, 7), 1, (0, 3), 17, 1),
+    (160, 192, (7, 1), 1, (3, 0), 17, 3),
+    (288, 384, 3, 2, 0, 35, 1),
+    (48, 64, 5, 1, 2, 35, 2),
+    (2048, 320, 1, 1, 0, 8, 1),
+]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("case", TMA_CASES, ids=[str(c) for c in TMA_CASES])
+def test_tma_im2col_equals_gather(case, dtype, monkeypatch, tmp_path):
+    """The TMA im2col activation loads deliver exactly the bytes the cp.async
+    gathers do (same smem tiles, same MMA order), so the two builds of the same
+    graph agree bit for bit, on every autotuned tile; batch > 1 covers the
+    image wrap inside a pixel tile."""
+    from paper_2312_10351_b200 import engine
+    cin, cout, k, s, p, hw, n = case
+    torch.manual_seed(0)
+    m = Wrap(cin, cout, k, s, p, hw).eval()
+    x = torch.randn(n, 3, hw, hw)
+    outs = []
+    monkeypatch.setenv("OPARA_TUNE_CACHE", str(tmp_path / "tune.json"))   # same tiles in both builds
+    for flag in ("1", "0"):
+        monkeypatch.setenv("OPARA_TMA", flag)
+        sg = engine.compile(m, x, device=0, profile_reps=2, dtype=dtype)
+        outs.append(sg.run(x.cuda()).clone())
+    assert torch.equal(outs[0], outs[1])
+    with torch.no_grad():
+        ref = m.double()(x.double())
+    rel = _rel(outs[0].permute(0, 3, 1, 2).float().cpu(), ref)
+    assert rel < (1e-5 if dtype == "f32" else 1.5e-2)
+
+
+class _StemReduce(nn.Module):
+    """Stem conv -> NASNet's factorized reduction (ReLU, stride-2 1x1 paths at
+    pixel offsets 0 and 1 of the zero-extended map, concatenated)."""
+
+    def __init__(self, cin, cout):
+        super().__init__()
+        from paper_2312_10351_b200 import zoo
+        self.stem = ConvBnRelu(3, cin, 1, 1, 0)
+        self.red = zoo._FactorizedReduction(cin, cout)
+
+    def forward(self, x):
+        return self.red(self.stem(x))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("hw", [21, 22, 83])
+def test_tma_im2col_subsample_paths(hw, dtype, monkeypatch, tmp_path):
+    """Offset-1 subsample convs have padding -1: their TMA box runs one pixel
+    past the edge (zeros, like the zero-extended map); odd and even sizes."""
+    from paper_2312_10351_b200 import engine
+    torch.manual_seed(0)
+    m = _StemReduce(64, 128).eval()
+    x = torch.randn(1, 3, hw, hw)
+    outs = []
+    monkeypatch.setenv("OPARA_TUNE_CACHE", str(tmp_path / "tune.json"))
+    for flag in ("1", "0"):
+        monkeypatch.setenv("OPARA_TMA", flag)
+        sg = engine.compile(m, x, device=0, profile_reps=2, dtype=dtype)
+        outs.append(sg.run(x.cuda()).clone())
+    assert torch.equal(outs[0], outs[1])
+    with torch.no_grad():
+        ref = m.double()(x.double())
+    rel = _rel(outs[0].permute(0, 3, 1, 2).float().cpu(), ref)
+    assert rel < (1e-5 if dtype == "f32" else 1.5e-2)
