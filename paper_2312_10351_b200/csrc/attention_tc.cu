@@ -1,14 +1,17 @@
-// Multi-head self-attention for one sequence, one CTA (8 warps) per head, on tcgen05:
+// Multi-head self-attention for one sequence, one CTA (16 warps) per head, on tcgen05:
 //   S = Q K^T          (tcgen05.mma kind::f16, M = 128 queries, N = 128 keys, K = 64)
 //   P = exp((S - max) * scale)   rows in registers straight from TMEM (tcgen05.ld)
 //   O = P V / rowsum   (tcgen05.mma, M = 128 queries, N = 64, K = 128 keys)
 // Q, K, V and O are channel views of [tokens][C] bf16 buffers (head h reads
-// columns off + h*64 ..); S and O accumulate in TMEM (fp32).  Operands are
-// staged in 64-byte-swizzled K-major atoms (Q, K by cp.async; V transposed on
-// the way in so the PV MMA reads K-major V^T; P written by the softmax warps).
-// Softmax: warps w and w + 4 share TMEM lane quarter w (query rows 32w..32w+31)
-// and split the 128 key columns in halves; row max and row sum are combined
-// through shared memory.  Shapes: tokens = 128, head_dim = 64 (BERT-base, seq 128).
+// columns off + h*64 ..); S and O accumulate in TMEM (fp32).  Every operand
+// is staged by cp.async straight from its natural row layout: Q, K as
+// 64-byte-swizzled K-major atoms, V as an MN-major operand (8-key x 32-d
+// atoms, MN atoms 512 B apart, key groups 1024 B apart; probed in
+// scripts/micro/umma_mn.cu), so no transpose pass; P is written by the
+// softmax warps.  Softmax: the four warps w, w+4, w+8, w+12 share TMEM lane
+// quarter w % 4 (query rows 32(w%4)..) and split the 128 keys in quarters;
+// row max and row sum are combined through shared memory.  Shapes: tokens =
+// 128, head_dim = 64 (BERT-base, seq 128).
 
 #include <cuda_bf16.h>
 
@@ -20,7 +23,7 @@
 namespace opara {
 namespace {
 
-constexpr int kT = 128, kD = 64, kThreads = 256;
+constexpr int kT = 128, kD = 64, kThreads = 512, kWarps = kThreads / 32;
 constexpr uint32_t kQBytes = kT * kD * 2, kKBytes = kT * kD * 2, kPBytes = kT * kT * 2, kVBytes = kD * kT * 2;
 
 struct AttnArgs {
@@ -41,6 +44,23 @@ __device__ __forceinline__ uint32_t sw64(int rows, int row, int c16) {
   return static_cast<uint32_t>(kb * rows * 64 + (row >> 3) * 512 + r8 * 64 + ((cw ^ ((r8 >> 1) & 3)) << 4));
 }
 
+// MN-major SW64 V operand: chunk c16 (d = 8 c16 ..) of key row `key`.
+constexpr uint32_t kVLbo = 512, kVSbo = 1024;   // MN atom stride, 8-key group stride
+__device__ __forceinline__ uint32_t vmn(int key, int c16) {
+  const int r = key & 7;
+  return static_cast<uint32_t>((c16 >> 2) * kVLbo + (key >> 3) * kVSbo + r * 64 + (((c16 & 3) ^ ((r >> 1) & 3)) << 4));
+}
+
+__device__ __forceinline__ uint64_t desc_mn_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;   // SWIZZLE_64B
+  return d;
+}
+
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -51,9 +71,10 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
   uint8_t* qs = smem;
   uint8_t* ks = qs + kQBytes;
   uint8_t* ps = ks + kKBytes;
-  uint8_t* vt = ps + kPBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(vt + kVBytes);  // [0] S ready, [1] O ready
+  uint8_t* vs = ps + kPBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vs + kVBytes);  // [0] S ready, [1] O ready
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  __shared__ float red_max[4][kT], red_sum[4][kT];
 
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -72,9 +93,9 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
 
   pdl_wait();
   trace_begin(trace);
-  // ---- stage Q, K (cp.async) and V (registers, all loads in flight at once);
-  // S = Q K^T is issued as soon as Q and K land, and V is transposed into the
-  // K-major V^T operand while the tensor core works on S.
+  // ---- stage Q, K (K-major) and V (MN-major): 3 x 1024 16-byte chunks, every
+  // copy in flight at once; S = Q K^T is issued once Q and K have landed,
+  // while V's group is still on the way
   const __nv_bfloat16* qg = a.q + a.q_off + h * kD;
   const __nv_bfloat16* kg = a.k + a.k_off + h * kD;
   const __nv_bfloat16* vg = a.v + a.v_off + h * kD;
@@ -85,19 +106,20 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
     cp_async16(tc::smem_u32(qs) + sw64(kT, row, c16), qg + static_cast<int64_t>(row) * a.q_stride + c16 * 8);
     cp_async16(tc::smem_u32(ks) + sw64(kT, row, c16), kg + static_cast<int64_t>(row) * a.k_stride + c16 * 8);
   }
-  uint4 vraw[kChunks];
+  asm volatile("cp.async.commit_group;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < kChunks; ++j) {
-    const int u = tid + j * kThreads, key = u >> 3, d0 = (u & 7) * 8;
-    vraw[j] = *reinterpret_cast<const uint4*>(vg + static_cast<int64_t>(key) * a.v_stride + d0);
+    const int u = tid + j * kThreads, key = u >> 3, c16 = u & 7;
+    cp_async16(tc::smem_u32(vs) + vmn(key, c16), vg + static_cast<int64_t>(key) * a.v_stride + c16 * 8);
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
   tc::fence_proxy_async_smem();
   __syncthreads();
 
   // ---- S = Q K^T
   constexpr uint32_t kIdS = tc::instr_desc(1, 128, 128);
-  constexpr uint32_t kIdO = tc::instr_desc(1, 128, 64);
+  constexpr uint32_t kIdO = tc::instr_desc(1, 128, 64) | (1u << 16);   // B (V) MN-major
   if (tid == 0) {
     tc::tc_fence_after();
 #pragma unroll
@@ -108,40 +130,35 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
     }
     tc::mma_commit(&bar[0]);
   }
-#pragma unroll
-  for (int j = 0; j < kChunks; ++j) {
-    const int u = tid + j * kThreads, key = u >> 3, d0 = (u & 7) * 8;
-    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&vraw[j]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i)  // V^T[d][key]: row d, k = key
-      *reinterpret_cast<__nv_bfloat16*>(vt + sw64(kD, d0 + i, key >> 3) + (key & 7) * 2) = e[i];
-  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");   // V landed (this thread's chunks)
+  tc::fence_proxy_async_smem();
   tc::mbar_wait(&bar[0], 0);
   tc::tc_fence_after();
 
-  // ---- softmax: thread = (query row, half of the key columns), 64 scores in registers
-  __shared__ float red_max[2][kT], red_sum[2][kT];
-  const int quarter = warp & 3, half = warp >> 2;
+  // ---- softmax: thread = (query row, quarter of the key columns), 32 scores in registers
+  const int quarter = warp & 3, kq = warp >> 2;
   const int q = quarter * 32 + lane;
   const uint32_t trow = static_cast<uint32_t>(quarter * 32) << 16;
-  constexpr int kHalf = kT / 2;
-  float sc[kHalf];
+  constexpr int kQuart = kT / 4;
+  float sc[kQuart];
+  {
+    float v0[16], v1[16];
+    tc::tmem_ld16x2(tS + trow + kq * kQuart, tS + trow + kq * kQuart + 16, v0, v1);
 #pragma unroll
-  for (int c8 = 0; c8 < kHalf / 8; ++c8) {
-    float v[8];
-    tc::tmem_ld8(tS + trow + half * kHalf + c8 * 8, v);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) sc[c8 * 8 + e] = v[e];
+    for (int e = 0; e < 16; ++e) {
+      sc[e] = v0[e];
+      sc[16 + e] = v1[e];
+    }
   }
   float mx = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < kHalf; ++j) mx = fmaxf(mx, sc[j]);
-  red_max[half][q] = mx;
+  for (int j = 0; j < kQuart; ++j) mx = fmaxf(mx, sc[j]);
+  red_max[kq][q] = mx;
   __syncthreads();
-  mx = fmaxf(red_max[0][q], red_max[1][q]);
+  mx = fmaxf(fmaxf(red_max[0][q], red_max[1][q]), fmaxf(red_max[2][q], red_max[3][q]));
   float sum = 0.f;
 #pragma unroll
-  for (int c16 = 0; c16 < kHalf / 8; ++c16) {
+  for (int c16 = 0; c16 < kQuart / 8; ++c16) {
     __nv_bfloat16 pv[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -150,13 +167,13 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
       sum += __bfloat162float(pb);  // normalise by exactly what the PV MMA consumes
       pv[e] = pb;
     }
-    *reinterpret_cast<uint4*>(ps + sw64(kT, q, half * (kHalf / 8) + c16)) = *reinterpret_cast<const uint4*>(pv);
+    *reinterpret_cast<uint4*>(ps + sw64(kT, q, kq * (kQuart / 8) + c16)) = *reinterpret_cast<const uint4*>(pv);
   }
-  red_sum[half][q] = sum;
+  red_sum[kq][q] = sum;
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
-  sum = red_sum[0][q] + red_sum[1][q];
+  sum = (red_sum[0][q] + red_sum[1][q]) + (red_sum[2][q] + red_sum[3][q]);
 
   // ---- O = P V
   if (tid == 0) {
@@ -164,23 +181,22 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
 #pragma unroll
     for (int s = 0; s < kT / 16; ++s) {
       tc::mma_f16(tO, tc::smem_desc_sw64(tc::smem_u32(ps) + (s >> 1) * kT * 64 + (s & 1) * 32, 512),
-                  tc::smem_desc_sw64(tc::smem_u32(vt) + (s >> 1) * kD * 64 + (s & 1) * 32, 512), kIdO, s != 0);
+                  desc_mn_sw64(tc::smem_u32(vs) + s * 2 * kVSbo, kVLbo, kVSbo), kIdO, s != 0);
     }
     tc::mma_commit(&bar[1]);
   }
   tc::mbar_wait(&bar[1], 0);
   tc::tc_fence_after();
+  // thread = (query row, 16 of the 64 head dims)
   const float inv = 1.f / sum;
-  __nv_bfloat16* og = a.out + static_cast<int64_t>(q) * a.out_stride + a.out_off + h * kD + half * (kD / 2);
+  float o[16];
+  tc::tmem_ld16x1(tO + trow + kq * 16, o);
+  __nv_bfloat16 ob[16];
 #pragma unroll
-  for (int c8 = 0; c8 < kD / 16; ++c8) {
-    float v[8];
-    tc::tmem_ld8(tO + trow + half * (kD / 2) + c8 * 8, v);
-    __nv_bfloat16 ob[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) ob[e] = __float2bfloat16_rn(v[e] * inv);
-    *reinterpret_cast<uint4*>(og + c8 * 8) = *reinterpret_cast<const uint4*>(ob);
-  }
+  for (int e = 0; e < 16; ++e) ob[e] = __float2bfloat16_rn(o[e] * inv);
+  __nv_bfloat16* og = a.out + static_cast<int64_t>(q) * a.out_stride + a.out_off + h * kD + kq * 16;
+  reinterpret_cast<uint4*>(og)[0] = reinterpret_cast<const uint4*>(ob)[0];
+  reinterpret_cast<uint4*>(og)[1] = reinterpret_cast<const uint4*>(ob)[1];
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) {
