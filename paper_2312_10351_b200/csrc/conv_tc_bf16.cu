@@ -53,7 +53,7 @@ __device__ unsigned g_phase_n;
       g_phase[slot][10] = ph[8];                                                                    \
       g_phase[slot][11] = ph[9];                                                                    \
       g_phase[slot][8] = (static_cast<unsigned long long>(a.M) << 40) | (static_cast<unsigned long long>(a.Cout) << 20) | a.K; \
-      g_phase[slot][9] = (static_cast<unsigned long long>(gridDim.x * gridDim.y * gridDim.z) << 32) | (static_cast<unsigned long long>(BN) << 24) | (nkb << 8) | (a.push ? 0x80 : 0) | (a.ws ? 0x40 : 0) | a.splits; \
+      g_phase[slot][9] = (static_cast<unsigned long long>(gridDim.x * gridDim.y * gridDim.z) << 32) | (static_cast<unsigned long long>(BN) << 24) | (nkb << 8) | (a.push ? 0x80 : 0) | a.splits; \
     }                                                                                               \
   } while (0)
 #else
@@ -110,16 +110,7 @@ struct BfArgs {
   int M, K, kblocks;
   int splits, kb_per_split;
   int push, rows_per;   // split-K reduction: 1 = partials pushed to the owner CTA (st.async)
-  int glob;             // split-K reduction through an L2 workspace + last-arrival CTA (no cluster)
-  float* ws;
-  unsigned* cnt;
   const int4* ktab;     // scalar gathers: per k (dr, dq, input offset) from the host (no divisions)
-  // fused residual + LayerNorm over all Cout channels (cluster spans the m-tiles)
-  int ln, res_cs;
-  const __nv_bfloat16* res;
-  const float* gamma;
-  const float* beta;
-  float eps;
   int64_t sN, sH, sW, sC;
 };
 
@@ -477,153 +468,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
   __syncwarp();
 
   // ------------------------------------------------------------ epilogue
-  if constexpr (BN == 16) if (a.ln) {   // (instantiated for the 16-wide tile only: BN fp32 values / thread)
-    // y = acc + bias + residual for this CTA's 128 channels x BN tokens, kept
-    // in registers (thread = channel); per-token sum / sum of squares over the
-    // CTA's channels -> smem; the cluster (one CTA per 128-channel tile)
-    // exchanges them over DSMEM; then normalise with gamma / beta and store.
-    float* part = reinterpret_cast<float*>(smem);               // [4 warps][BN][2]
-    float* cta_part = part + 4 * BN * 2;                        // [BN][2] this CTA's channel sums
-    float* stats = cta_part + BN * 2;                           // [BN][2] mean, rstd
-    const int ch = mt * 128 + (warp & 3) * 32 + lane;
-    const bool ch_ok = ch < a.Cout;
-    float y[BN];
-    if (warp < 4) {
-      tc::mbar_wait(accum, 0);
-      tc::tc_fence_after();
-      if (tid == 0) PHASE(4);
-      const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-      const float b = (a.bias && ch_ok) ? __ldg(a.bias + ch) : 0.f;
-#pragma unroll
-      for (int c8 = 0; c8 < BN / 8; ++c8) {
-        float v[8];
-        tc::tmem_ld8(trow + c8 * 8, v);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int p = n0 + c8 * 8 + e;
-          const float r = (ch_ok && p < a.M) ? __bfloat162float(a.res[static_cast<int64_t>(p) * a.res_cs + ch]) : 0.f;
-          y[c8 * 8 + e] = ch_ok ? v[e] + b + r : 0.f;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < BN; ++j) {
-        const float s1 = warp_sum(y[j]), s2 = warp_sum(y[j] * y[j]);
-        if (lane == 0) {
-          part[(warp * BN + j) * 2] = s1;
-          part[(warp * BN + j) * 2 + 1] = s2;
-        }
-      }
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    if (warp == kTmemWarp) {
-      tc::tc_fence_after();
-      tc::tmem_dealloc(tmem, kTmemCols);
-    }
-    if (tid < BN) {
-      float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        s1 += part[(w * BN + tid) * 2];
-        s2 += part[(w * BN + tid) * 2 + 1];
-      }
-      cta_part[tid * 2] = s1;
-      cta_part[tid * 2 + 1] = s2;
-    }
-    tc::cluster_sync();
-    if (tid < BN) {
-      const int ntiles = static_cast<int>(gridDim.y);
-      float s1 = 0.f, s2 = 0.f;
-      const uint32_t cp = tc::smem_u32(cta_part + tid * 2);
-      for (int r = 0; r < ntiles; ++r) {   // cluster rank r = m-tile r (cluster spans gridDim.y)
-        float v0, v1;
-        asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v0), "=f"(v1) : "r"(tc::map_cluster(cp, r)));
-        s1 += v0;
-        s2 += v1;
-      }
-      const float mean = s1 / a.Cout;
-      const float var = fmaxf(s2 / a.Cout - mean * mean, 0.f);
-      stats[tid * 2] = mean;
-      stats[tid * 2 + 1] = rsqrtf(var + a.eps);
-    }
-    __syncthreads();
-    if (warp < 4 && ch_ok) {
-      const float g = __ldg(a.gamma + ch), bb = __ldg(a.beta + ch);
-      TO* out = static_cast<TO*>(a.out);
-#pragma unroll
-      for (int j = 0; j < BN; ++j) {
-        const int p = n0 + j;
-        if (p < a.M) {
-          const float o = (y[j] - stats[j * 2]) * stats[j * 2 + 1] * g + bb;
-          TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
-          if constexpr (std::is_same<TO, float>::value) *dst = o;
-          else *dst = __float2bfloat16_rn(o);
-        }
-      }
-    }
-    tc::cluster_sync();   // peers may still be reading this CTA's channel sums
-    PHASE_FLUSH();
-    trace_end(trace);
-    return;
-  }
-  if (a.glob) {
-    // Split-K through L2 without a cluster: every split stores its partial
-    // [BN][128] tile to the workspace (coalesced along channels), the last CTA
-    // to arrive on the tile's counter sums the splits in z order (deterministic)
-    // and runs the epilogue; no cluster launch, no DSMEM, no co-scheduling.
-    const int tiles = gridDim.x * gridDim.y, tile = blockIdx.x + blockIdx.y * gridDim.x;
-    const int64_t plane = static_cast<int64_t>(BN) * 128;
-    if (warp < 4) {
-      tc::mbar_wait(accum, 0);
-      tc::tc_fence_after();
-      if (tid == 0) PHASE(4);
-      const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-      float* mine = a.ws + (static_cast<int64_t>(blockIdx.z) * tiles + tile) * plane + warp * 32 + lane;
-#pragma unroll 4
-      for (int c8 = 0; c8 < BN / 8; ++c8) {
-        float v[8];
-        tc::tmem_ld8(trow + c8 * 8, v);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) __stcg(mine + (c8 * 8 + e) * 128, v[e]);
-      }
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    if (warp == kTmemWarp) {
-      tc::tc_fence_after();
-      tc::tmem_dealloc(tmem, kTmemCols);
-    }
-    if (!splitk_arrive_last(a.cnt + tile, a.splits)) {
-      PHASE_FLUSH();
-    trace_end(trace);
-      return;
-    }
-    TO* out = static_cast<TO*>(a.out);
-    for (int idx = tid; idx < BN * 32; idx += kThreads) {
-      const int col = idx >> 5, r4 = (idx & 31) * 4;
-      const int p = n0 + col, ch0 = mt * 128 + r4;
-      if (p >= a.M) continue;
-      const float* src = a.ws + static_cast<int64_t>(tile) * plane + col * 128 + r4;
-      float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
-      for (int z = 1; z < a.splits; ++z) {
-        const float4 q = __ldcg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(z) * tiles * plane));
-        acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
-      }
-      const float y[4] = {acc.x, acc.y, acc.z, acc.w};
-      TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (ch0 + e < a.Cout) {
-          const float o = act_fn(y[e] + (a.bias ? __ldg(a.bias + ch0 + e) : 0.f), a.act);
-          if constexpr (std::is_same<TO, float>::value) dst[e] = o;
-          else dst[e] = __float2bfloat16_rn(o);
-        }
-      }
-    }
-    PHASE_FLUSH();
-    trace_end(trace);
-    return;
-  }
   if (push) {
     // TMEM -> registers -> this CTA's smem (the drained ring), laid out as one
     // contiguous [128 channels][rows_per] block per owning rank; then one
@@ -944,40 +788,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   a.vec_out = (a.out_cs % 4 == 0 && a.out_coff % 4 == 0 && reinterpret_cast<uintptr_t>(a.out) % align == 0) ? 1 : 0;
   const BfVariant* v = bf_variants();
   const int mtiles = (a.Cout + 127) / 128;
-  a.ktab = (op.i[27] == 0) ? static_cast<const int4*>(op.p[5]) : nullptr;
-  a.ln = static_cast<int>(op.i[27]);
-  a.res = static_cast<const __nv_bfloat16*>(op.p[4]);
-  a.res_cs = static_cast<int>(op.i[28]);
-  a.gamma = static_cast<const float*>(op.p[5]);
-  a.beta = static_cast<const float*>(op.p[6]);
-  a.eps = static_cast<float>(op.f[0]);
-  if (a.ln) {
-    // fused residual + LayerNorm: no split-K, one cluster of all m-tiles per
-    // token tile; the 16-wide deep-ring tile streams its whole weight slice
-    // into smem before griddepcontrol.wait
-    if (mtiles > 8) return fail(OPARA_ERR_VALUE, "conv2d_tc_bf16 LayerNorm epilogue: Cout must be <= 1024");
-    if (mode == kScalarF32 || !a.res || !a.gamma || !a.beta) {
-      if (!dry) return fail(OPARA_ERR_VALUE, "conv2d_tc_bf16 LayerNorm epilogue: bf16 input, residual, gamma, beta");
-    }
-    const int lid = 4;   // the epilogue is instantiated for the 16-wide deep-ring tile
-    a.splits = 1;
-    a.kb_per_split = a.kblocks;
-    a.push = 0;
-    a.glob = 0;
-    a.rows_per = v[lid].bn;
-    LaunchCfg c;
-    c.func = v[lid].func[mode][out_f32 ? 1 : 0];
-    c.grid = dim3(ceil_div(a.M, v[lid].bn), mtiles, 1);
-    c.block = dim3(kThreads);
-    c.smem = v[lid].smem;
-    if (cfg) *cfg = c;
-    if (dry) return OPARA_OK;
-    opara_status st = set_attr_once(c.func, attr_smem(v[lid].smem));
-    if (st != OPARA_OK) return st;
-    if (!encode(v[lid].bn)) return fail(OPARA_ERR_CUDA, "conv2d_tc_bf16: cuTensorMapEncodeIm2col failed");
-    void* args[] = {&a, &trace};
-    return launch_kernel_cluster(c, args, s, dim3(1, static_cast<unsigned>(mtiles), 1));
-  }
+  a.ktab = static_cast<const int4*>(op.p[5]);
   int id = op.variant;
   if (id < 0 || id > 4) {   // 0..3: tile width 32 << id, 4: width 16 (deep weight ring)
     id = 0;
@@ -999,7 +810,7 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   splits = std::min<int64_t>(splits, std::max(1, a.kblocks / 2));
   splits = std::max<int64_t>(1, splits);
   const void* func = v[id].func[mode][out_f32 ? 1 : 0];
-  if (splits > 1 && op.i[19] <= 1 && op.i[26] != 2)   // (the L2 reduction needs no co-resident cluster)
+  if (splits > 1 && op.i[19] <= 1)
     while (splits > 1) {
       const int rp = ((bn + static_cast<int>(splits) - 1) / static_cast<int>(splits) + 3) / 4 * 4;
       const size_t rb = static_cast<size_t>(splits) * 128 * rp * 4;
@@ -1017,30 +828,18 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
   a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
             op.i[26] == 0) ? 1 : 0;
-  a.glob = (a.splits > 1 && op.i[26] == 2) ? 1 : 0;   // reduction through an L2 workspace
   LaunchCfg c;
   c.func = func;
   c.grid = dim3(ceil_div(a.M, bn), mtiles, a.splits);
   c.block = dim3(kThreads);
   c.smem = v[id].smem + (a.push ? recv_bytes : 0);
-  const int64_t tiles = static_cast<int64_t>(c.grid.x) * c.grid.y;
-  const int64_t ws_floats = a.glob ? static_cast<int64_t>(a.splits) * tiles * bn * 128 : 0;
-  c.workspace = a.glob ? splitk_workspace_bytes(ws_floats, tiles) : 0;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
-  if (a.glob) {
-    if (!op.p[7]) return fail(OPARA_ERR_INTERNAL, "conv2d_tc_bf16: split-K workspace missing");
-    a.ws = static_cast<float*>(op.p[7]);
-    a.cnt = splitk_counters(op.p[7], ws_floats);
-  } else {
-    a.ws = nullptr;
-    a.cnt = nullptr;
-  }
   opara_status st = set_attr_once(func, attr_smem(v[id].smem));
   if (st != OPARA_OK) return st;
   if (!encode(bn)) return fail(OPARA_ERR_CUDA, "conv2d_tc_bf16: cuTensorMapEncodeIm2col failed");
   void* args[] = {&a, &trace};
-  return launch_kernel(c, args, s, (a.splits > 1 && !a.glob) ? static_cast<unsigned>(a.splits) : 1u);
+  return launch_kernel(c, args, s, a.splits > 1 ? static_cast<unsigned>(a.splits) : 1u);
 }
 
 }  // namespace opara

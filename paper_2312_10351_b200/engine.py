@@ -204,7 +204,7 @@ def concurrency_targets(program: Program, num_sms: int = 148, scale: float = 1.0
     return out
 
 
-SPLITK_MODES = {"push": 0, "pull": 1, "global": 2}
+SPLITK_MODES = {"push": 0, "pull": 1}
 
 
 def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0,
@@ -338,9 +338,8 @@ class ScheduledGraph:
         recs = (_lib.OparaOp * len(program.ops))()
         self.bound_grids = bool(bound_grids)
         self.bound_scale = bound_scale
-        # split-K reduction: "push" (st.async partials to the owner CTA), "pull" (DSMEM after a
-        # cluster barrier), "global" (bf16 engine: partials through an L2 workspace, last CTA
-        # reduces, no cluster), or "auto": pull where other convs share the DAG level
+        # split-K reduction: "push" (partials bulk-copied to the owner CTA), "pull" (DSMEM after a
+        # cluster barrier), or "auto": pull where other convs share the DAG level
         # (concurrent branches), push for convs that run alone
         self.splitk = splitk
         conc = concurrent_convs(program) if splitk == "auto" else {}
@@ -354,17 +353,10 @@ class ScheduledGraph:
                 recs[k] = _op_record(op, self._views(op), self._weights(op),
                                      conv_engine_for(op, self.conv_engine), self.targets.get(k, 0),
                                      mode_of[k])
-                if op.kind == CONV2D and recs[k].i[22] == 2 and not op.ints.get("ln"):
+                if op.kind == CONV2D and recs[k].i[22] == 2:
                     ktab = self._gather_table(op)
                     if ktab is not None:
                         recs[k].p[5] = ktab
-                if op.kind == CONV2D and op.ints.get("ln"):   # fused residual + LayerNorm epilogue
-                    (rb, rcoff, rcs, _), = self._all_views(op)[1:2]
-                    arr = self._arrays(op)
-                    recs[k].i[27], recs[k].i[28] = 1, rcs
-                    recs[k].p[4] = _at(rb, rcoff, 2)
-                    recs[k].p[5], recs[k].p[6] = arr["gamma"], arr["beta"]
-                    recs[k].f[0] = op.floats[0]
         self.debug_ts = {}
         if os.environ.get("OPARA_CONV_DEBUG"):  # per-phase timestamps of CTA 0 (conv_tc.cu)
             for k, op in enumerate(program.ops):
@@ -502,7 +494,7 @@ class ScheduledGraph:
         L = _lib.lib()
         groups: dict[tuple, list[int]] = {}
         for k, op in enumerate(self.program.ops):
-            if op.kind == CONV2D and recs[k].i[22] in (1, 2) and not recs[k].i[27]:
+            if op.kind == CONV2D and recs[k].i[22] in (1, 2):
                 key = self._tune_key(recs[k]) + (self.targets.get(k, 0),)
                 groups.setdefault(key, []).append(k)
         cache_path = os.environ.get("OPARA_TUNE_CACHE")
@@ -827,7 +819,7 @@ class ScheduledGraph:
 
 
 def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "opara",
-            dtype: str = "f32", fuse_layernorm: bool = False,
+            dtype: str = "f32",
             gpu_config: GpuConfig | None = None, profile_reps: int = 20,
             seed: int | None = None, conv_engine: str = "tc",
             bound_grids: bool | str = False, tune: bool = True,
@@ -847,7 +839,7 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
         import warnings
         warnings.warn("CUDA context created before CUDA_DEVICE_MAX_CONNECTIONS=32 was set: "
                       "concurrent plan streams share fewer hardware queues", RuntimeWarning)
-    program = lower(model, example, dtype, fuse_layernorm)
+    program = lower(model, example, dtype)
     if bound_grids != "auto":
         # measured default: pull reductions pair with bounded grids, push with full grids
         splitk = splitk or ("pull" if bound_grids else "push")

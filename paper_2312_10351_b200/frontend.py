@@ -35,7 +35,6 @@ FIELD_EMBEDDING, FIRST_ORDER, PACK_INPUT = 16, 17, 18
 # linear + residual + LayerNorm fusion (opt-in): deepest reduction (K) one CTA streams whole.
 # Measured on BERT-base: the fused O-proj + LN (48 unsplit CTAs streaming 196 KB of weights
 # each) takes 10.7 us against 5.3 + 1.7 us unfused, so compile() leaves it off by default.
-LN_FUSE_MAX_K = int(__import__("os").environ.get("OPARA_LN_FUSE_MAX_K", "4096"))
 
 # fused activations (csrc kernels): 0 none, 1 ReLU, 2 GELU (erf), 3 tanh, 4 sigmoid
 ACT_NONE, ACT_RELU, ACT_GELU, ACT_TANH, ACT_SIGMOID = 0, 1, 2, 3, 4
@@ -137,9 +136,8 @@ def _fold_bn(conv: nn.Conv2d, bn: nn.BatchNorm2d | None):
 
 
 class _Lowerer:
-    def __init__(self, gm: fx.GraphModule, dtype: str = "f32", fuse_layernorm: bool = False):
+    def __init__(self, gm: fx.GraphModule, dtype: str = "f32"):
         self.gm = gm
-        self.fuse_layernorm = fuse_layernorm   # linear + residual + LayerNorm -> one GEMM op (bf16)
         self.act_dtype = dtype          # element type of conv / pool activations
         self.esize = 2 if dtype == "bf16" else 4
         self.ops: list[LoweredOp] = []
@@ -517,26 +515,10 @@ class _Lowerer:
         bias = (b if b is not None else torch.zeros(nout)).numpy()
         ints = dict(N=1, H=1, W=t, Cin=k, OH=1, OW=t, Cout=nout, R=1, S=1, sh=1, sw=1, ph=0, pw=0,
                     relu=int(act == 1), act=act)
-        inputs, arrays, floats = [x], {}, ()
-        ln = self._single_user(node, lambda u: u.op == "call_function" and
-                               getattr(u.target, "__name__", "") == "add_layer_norm" and u.args[0] is node)
-        if (act == 0 and ln is not None and self.act_dtype == "bf16" and self.fuse_layernorm
-                and nout <= 1024 and nout % 128 == 0 and k <= LN_FUSE_MAX_K):
-            # linear -> residual add -> LayerNorm in one op: the GEMM's epilogue adds
-            # the residual and normalises each token over all output channels
-            res = self.value(ln.args[1])
-            inputs = [x, res]
-            arrays = {"gamma": self._param(ln.args[2]).numpy(), "beta": self._param(ln.args[3]).numpy()}
-            floats = (float(ln.args[4]),)
-            ints["ln"] = 1
-            self.consumed.add(ln)
-            tail = ln
         out = self.new_tensor((1, 1, t, nout))
-        op = LoweredOp(CONV2D, "gemm", OpClass.COMPUTE, ints, inputs, out, w.t().contiguous().numpy(), bias,
-                       flops=2 * t * k * nout + (8 * t * nout if ints.get("ln") else 0),
-                       bytes_min=self.esize * (t * k + k * nout + t * nout) + 4 * nout
-                       + (self.esize * t * nout if ints.get("ln") else 0),
-                       label=node.name, arrays=arrays, floats=floats)
+        op = LoweredOp(CONV2D, "gemm", OpClass.COMPUTE, ints, [x], out, w.t().contiguous().numpy(), bias,
+                       flops=2 * t * k * nout, bytes_min=self.esize * (t * k + k * nout + t * nout) + 4 * nout,
+                       label=node.name)
         self.emit(op)
         self.env[tail] = out
 
@@ -757,18 +739,16 @@ class _Lowerer:
         return Program(self.ops, self.tensors, inputs[0], outs[0], sorted(edges), outs, inputs)
 
 
-def lower(model: nn.Module, example, dtype: str = "f32", fuse_layernorm: bool = False) -> Program:
+def lower(model: nn.Module, example, dtype: str = "f32") -> Program:
     """Trace `model` with torch.fx and lower it to executor operators.
 
     `example` is one input tensor or a tuple of them (one per forward
     argument).  dtype "f32": fp32 activations end to end (3xTF32 tensor-core
     convs).  dtype "bf16": bf16 activations and weights with fp32
     accumulation; the graph input stays fp32 NCHW and the classifier head
-    stays fp32.  fuse_layernorm: a bf16 linear whose only consumer is
-    add_layer_norm(linear, residual) becomes one GEMM with a residual +
-    LayerNorm epilogue."""
+    stays fp32."""
     if dtype not in ("f32", "bf16"):
         raise ValueError(f"unknown dtype {dtype!r}")
     model = model.eval()
     gm = fx.symbolic_trace(model)
-    return _Lowerer(gm, dtype, fuse_layernorm).run(example)
+    return _Lowerer(gm, dtype).run(example)

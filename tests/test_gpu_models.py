@@ -112,25 +112,10 @@ def test_nasnet_large_parity(dtype, tol):
     assert rel <= tol, rel
 
 
-def test_bert_fused_layernorm_epilogue_parity():
-    """Opt-in linear + residual + LayerNorm fusion (one GEMM whose cluster spans
-    every 128-channel tile and exchanges per-token sums over DSMEM) matches
-    the HF forward within the bf16 tolerance."""
-    from paper_2312_10351_b200 import engine, zoo
-    model, ref_model, ids = zoo.build_bert()
-    sg = engine.compile(model, ids, device=0, profile_reps=2, dtype="bf16", fuse_layernorm=True)
-    assert sum(1 for op in sg.program.ops if op.ints.get("ln")) == 24
-    hidden, pooled = sg.run(ids.cuda())
-    with torch.no_grad():
-        ref_h, ref_p = ref_model.cuda()(ids.cuda())
-    assert _rel(hidden.float().reshape(ref_h.shape), ref_h) < 1e-2
-    assert _rel(pooled.float().reshape(ref_p.shape), ref_p) < 1e-2
-
-
-@pytest.mark.parametrize("splitk", ["push", "pull", "global", "auto"])
+@pytest.mark.parametrize("splitk", ["push", "pull", "auto"])
 def test_splitk_reductions_agree(splitk):
-    """Every split-K reduction (st.async push to the owner CTA, DSMEM pull after
-    a cluster barrier, L2 workspace + last-arrival CTA, per-level auto) gives
+    """Every split-K reduction (bulk-copy push to the owner CTA, DSMEM pull after
+    a cluster barrier, per-level auto) gives
     the same network output within the bf16 tolerance, and each graph pair
     (Opara / sequential) is bit-identical."""
     from paper_2312_10351_b200 import engine, zoo
