@@ -619,6 +619,10 @@ def _ncu_traffic(args, dom: str):
         vals, shape = {}, None
         for ln in prof.read_text().splitlines():
             parts = [x.strip() for x in ln.split("|")]
+            if len(parts) > 3 and parts[1] == f"family dram bytes per launch: {dom}":
+                # mean over every launch of the family in one timed step (launch list pass)
+                return int(float(parts[3])), (f"dram read+write bytes per {dom} launch, averaged over every "
+                                              f"launch of one timed step (ncu launch-list pass, {prof.name})")
             if len(parts) > 3 and parts[1].startswith("dram__bytes_"):
                 mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(parts[2], 1)
                 vals[parts[1]] = float(parts[3]) * mult

@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(const __grid_con
         for (int i = 0; i < nkb; ++i) {
           const int s = i % kStages;
           if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+          if (dbg && i < 64) a.dbg[768 + i] = global_ns();
           tc::mbar_arrive_expect_tx(&landed[s], kXBytes);
           tc::tma_im2col_4d(smem + s * kStage + 2 * kWBytes, &a.tmap, dc, w0, h0, b, dq, dr, &landed[s]);
           dc += kBKF;

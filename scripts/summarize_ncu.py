@@ -20,8 +20,11 @@ rows = list(csv.reader(launches.open()))
 hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
 hdr, data = rows[hi], rows[hi + 1:]
 ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+imn = hdr.index("Metric Name")
 scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+bscale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6}
 tot, cnt = collections.defaultdict(float), collections.Counter()
+dram = collections.defaultdict(float)   # kernel family -> dram read + write bytes (all launches)
 
 
 def is_ours(name: str) -> bool:   # libopara kernels live in opara::(anonymous namespace)
@@ -30,6 +33,10 @@ def is_ours(name: str) -> bool:   # libopara kernels live in opara::(anonymous n
 ours = []
 for r in data:
     name = r[ik].split("(")[0].replace("void ", "")
+    metric = r[imn]
+    if metric.startswith("dram__bytes_"):
+        dram[name] += float(r[iv].replace(",", "")) * bscale.get(r[iu], 1)
+        continue
     v = float(r[iv].replace(",", "")) * scale[r[iu]]
     tot[name] += v
     cnt[name] += 1
@@ -37,19 +44,26 @@ for r in data:
         ours.append((r[0], name, r[hdr.index("Grid Size")], r[hdr.index("Block Size")], f"{v:.3f}"))
 T_ours = sum(v for k, v in tot.items() if is_ours(k))
 lines.append(f"# ncu launch list — {tag}\n")
-lines.append(f"Source: `{launches.name}` (`ncu --metrics gpu__time_duration.sum --clock-control none`, "
-             "cold-cache and serialised per launch: compare SHARES, not absolutes), captured inside the "
-             "bench's timed region only (`--profile-region`: cudaProfilerStart/Stop around the Opara "
-             "replays), so every row is a libopara kernel.\n")
-lines.append("| share of our kernel time | total us | launches | kernel |\n|---:|---:|---:|---|")
+lines.append(f"Source: `{launches.name}` (`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+             "dram__bytes_write.sum --clock-control none`, cold-cache and serialised per launch: compare SHARES, "
+             "not absolutes), captured inside the bench's timed region only (`--profile-region`: "
+             "cudaProfilerStart/Stop around the Opara replays), so every row is a libopara kernel.\n")
+lines.append("| share of our kernel time | total us | launches | DRAM MB per launch | kernel |\n|---:|---:|---:|---:|---|")
 for k, v in sorted(tot.items(), key=lambda x: -x[1]):
     if is_ours(k):
-        lines.append(f"| {v / T_ours * 100:5.1f}% | {v:10.1f} | {cnt[k]:5d} | `{k}` |")
+        dm = f"{dram[k] / cnt[k] / 1e6:.3f}" if k in dram else "-"
+        lines.append(f"| {v / T_ours * 100:5.1f}% | {v:10.1f} | {cnt[k]:5d} | {dm} | `{k}` |")
 (out / f"{tag}_launches.md").write_text("\n".join(lines) + "\n")
 with (out / f"{tag}_launches_ours.csv").open("w", newline="") as f:
     w = csv.writer(f)
     w.writerow(["id", "kernel", "grid", "block", "gpu_time_us"])
     w.writerows(ours)
+# per-family DRAM traffic per launch (template arguments folded: the bench's roofline names families)
+fam_b, fam_n = collections.defaultdict(float), collections.Counter()
+for k, v in dram.items():
+    f = k.split("<")[0].split("::")[-1]
+    fam_b[f] += v
+    fam_n[f] += cnt[k]
 
 # full capture
 raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -72,6 +86,8 @@ full = [f"# ncu --set full — {tag}\n", f"Source: `{rep.name}` (one launch; `--
 for k in keys:
     if k in d:
         full.append(f"| {k} | {d[k][0]} | {d[k][1]} |")
+for f in sorted(fam_b):
+    full.append(f"| family dram bytes per launch: {f} | byte | {fam_b[f] / max(fam_n[f], 1):.0f} |")
 full.append("\nWarp stall reasons (pc sampling):\n\n| share | reason |\n|---:|---|")
 for k, x in sorted(st, key=lambda t: -t[1])[:10]:
     full.append(f"| {x / tot_s * 100:.1f}% | {k.replace('smsp__pcsamp_warps_issue_stalled_', '')} |")

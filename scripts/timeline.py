@@ -7,6 +7,7 @@ and an ASCII Gantt of the first kernels by plan stream).
     python scripts/timeline.py MODEL [DTYPE] [--batch B]
 """
 import argparse
+import os
 import sys
 from pathlib import Path
 
@@ -64,6 +65,6 @@ for nid, s, e in tr:
     b = max(a + 1, int((e - t0) / (t1 - t0) * width))
     lines.append(f"s{sg.plan.assignment[nid]:<3d} {sg.program.ops[nid - 1].name:10s} |" + " " * a + "#" * (b - a))
 lines.append("```")
-out = Path("gpurun_out") / f"r01_{args.model}_{args.dtype}_timeline.md"   # copied into profiles/
+out = Path("gpurun_out") / f"{os.environ.get('OPARA_ROUND', 'r02')}_{args.model}_{args.dtype}_timeline.md"   # copied into profiles/
 out.write_text("\n".join(lines) + "\n")
 print("\n".join(lines[:8]))
