@@ -69,6 +69,8 @@ struct TcArgs {
   int M, K, kblocks;
   int splits, kb_per_split;
   int push, rows_per;   // split-K reduction: 1 = partials pushed to the owner CTA (st.async)
+  int l2red;            // split-K reduction through L2: partial tiles in `ws`, one cluster barrier
+  float* ws;
   int64_t sN, sH, sW, sC;
 };
 
@@ -475,6 +477,68 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(const __grid_con
     DBG(6);
     if (tid == 0) tc::bulk_wait_read();   // the source blocks stay valid until the engine has read them
     DBG(7);
+    trace_end(trace);
+    return;
+  }
+  if (a.l2red) {
+    // Split-K through L2: each rank stores its partial [BN][128] tile to its
+    // workspace slice (coalesced along channels), one cluster barrier
+    // (release / acquire at cluster scope orders the global stores), then
+    // rank r reduces rows [r*BN/S, (r+1)*BN/S) from every slice in rank order
+    // (deterministic).  The smem ports carry nothing: the DSMEM pull moved
+    // each tile twice through them (~17-21 B/clk per SM) and measured ~2.4 us.
+    const int tiles = gridDim.x * gridDim.y, tile_id = blockIdx.x + blockIdx.y * gridDim.x;
+    const int64_t plane = static_cast<int64_t>(BN) * 128;
+    if (warp < kProducerWarps) {
+      tc::mbar_wait(accum, 0);
+      tc::tc_fence_after();
+      DBG(4);
+      const int quarter = warp & 3, half = warp >> 2;
+      const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+      float* mine = a.ws + (static_cast<int64_t>(blockIdx.z) * tiles + tile_id) * plane + quarter * 32 + lane;
+      drain_accumulators<BN, kAcc>(trow, half, [&](int col, float val) { __stcg(mine + col * 128, val); });
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    if (warp == kMmaWarp) {
+      tc::tc_fence_after();
+      tc::tmem_dealloc(tmem, kTmemCols);
+    }
+    DBG(5);
+    const int splits = a.splits;
+    const int rows_per = (BN + splits - 1) / splits;
+    const int r0 = static_cast<int>(blockIdx.z) * rows_per, r1 = min(min(BN, r0 + rows_per), a.M - n0);
+    const float* base = a.ws + static_cast<int64_t>(tile_id) * plane + lane * 4;
+    const int64_t zstride = static_cast<int64_t>(tiles) * plane;
+    for (int row = r0 + warp; row < r1; row += kThreads / 32) {
+      float4 part[kMaxSplits];   // every rank's load in flight before the first add
+#pragma unroll
+      for (int z = 0; z < kMaxSplits; ++z)
+        if (z < splits) part[z] = __ldcg(reinterpret_cast<const float4*>(base + z * zstride + row * 128));
+      float4 acc = part[0];
+#pragma unroll
+      for (int z = 1; z < kMaxSplits; ++z)
+        if (z < splits) {
+          acc.x += part[z].x; acc.y += part[z].y; acc.z += part[z].z; acc.w += part[z].w;
+        }
+      acc.x += bias4.x; acc.y += bias4.y; acc.z += bias4.z; acc.w += bias4.w;
+      if (a.relu) {
+        acc.x = apply_act(acc.x, a.relu); acc.y = apply_act(acc.y, a.relu);
+        acc.z = apply_act(acc.z, a.relu); acc.w = apply_act(acc.w, a.relu);
+      }
+      float* dst = a.out + static_cast<int64_t>(n0 + row) * a.out_cs + a.out_coff + ch;
+      if (a.vec_out && ch + 3 < a.Cout) {
+        *reinterpret_cast<float4*>(dst) = acc;
+      } else {
+        if (ch + 0 < a.Cout) dst[0] = acc.x;
+        if (ch + 1 < a.Cout) dst[1] = acc.y;
+        if (ch + 2 < a.Cout) dst[2] = acc.z;
+        if (ch + 3 < a.Cout) dst[3] = acc.w;
+      }
+    }
+    DBG(6);
+    DBG(7);
+    if (a.dbg && tid == 0 && cta_lin < 96) a.dbg[64 + 2 * cta_lin + 1] = global_ns();
     trace_end(trace);
     return;
   }
@@ -1001,13 +1065,20 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
   a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
             op.i[26] == 0) ? 1 : 0;
+  a.l2red = (a.splits > 1 && op.i[26] == 2) ? 1 : 0;
+  a.ws = nullptr;
   LaunchCfg c;
   c.func = func;
   c.grid = dim3(ceil_div(a.M, v[id].bn), (a.Cout + 127) / 128, a.splits);
   c.block = dim3(kThreads);
   c.smem = v[id].smem + (a.push ? recv_bytes : 0);
+  c.workspace = a.l2red ? static_cast<size_t>(c.grid.x) * c.grid.y * c.grid.z * v[id].bn * 128 * 4 : 0;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
+  if (a.l2red) {
+    if (!op.p[7]) return fail(OPARA_ERR_INTERNAL, "conv2d_tc: split-K workspace missing");
+    a.ws = static_cast<float*>(op.p[7]);
+  }
   opara_status st = set_smem_attr(v[id]);
   if (st != OPARA_OK) return st;
   if (tma && !make_im2col_map(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, op.p[0], a.N, a.H, a.W, a.Cin, in_cs,

@@ -110,6 +110,8 @@ struct BfArgs {
   int M, K, kblocks;
   int splits, kb_per_split;
   int push, rows_per;   // split-K reduction: 1 = partials pushed to the owner CTA (st.async)
+  int l2red;            // split-K reduction through L2 (partial tiles in `ws`, one cluster barrier)
+  float* ws;
   const int4* ktab;     // scalar gathers: per k (dr, dq, input offset) from the host (no divisions)
   int64_t sN, sH, sW, sC;
 };
@@ -560,12 +562,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
     tc::tc_fence_after();
     if (tid == 0) PHASE(4);
     const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    // L2 reduction: the partial goes to this rank's workspace slice instead
+    // of smem (the DSMEM pull moves each tile twice through the smem ports)
+    float* mine = a.l2red ? a.ws + (static_cast<int64_t>(blockIdx.z) * gridDim.x * gridDim.y + blockIdx.x +
+                                    blockIdx.y * gridDim.x) * BN * 128 + warp * 32 + lane
+                          : nullptr;
 #pragma unroll 4
     for (int c8 = 0; c8 < BN / 8; ++c8) {
       float v[8];
       tc::tmem_ld8(trow + c8 * 8, v);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) tile[(c8 * 8 + e) * 128 + warp * 32 + lane] = v[e];
+      for (int e = 0; e < 8; ++e) {
+        if (a.l2red) __stcg(mine + (c8 * 8 + e) * 128, v[e]);
+        else tile[(c8 * 8 + e) * 128 + warp * 32 + lane] = v[e];
+      }
     }
     if (tid == 0) PHASE(8);
   }
@@ -587,6 +597,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
   const int rows_per = (BN + splits - 1) / splits;
   const int r0 = rank * rows_per, r1 = min(BN, r0 + rows_per);
   const uint32_t tile_s = tc::smem_u32(tile);
+  const int64_t zstride = static_cast<int64_t>(gridDim.x) * gridDim.y * BN * 128;
+  const float* l2base = a.l2red ? a.ws + (static_cast<int64_t>(blockIdx.x + blockIdx.y * gridDim.x)) * BN * 128 + lane * 4
+                                : nullptr;
   TO* out = static_cast<TO*>(a.out);
   // a row per warp iteration, every split's DSMEM load issued before the first add
   constexpr int kRB = 1, kWarps = kThreads / 32;   // (2 rows in flight measured slower: Inception 0.390 -> 0.402 ms)
@@ -602,7 +615,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
       if (splits > 1) {
 #pragma unroll
         for (int z = 0; z < kMaxSplits; ++z)
-          if (z < splits) part[rb][z] = tc::ld_dsmem_f4(tc::map_cluster(tile_s + off, z));
+          if (z < splits)
+            part[rb][z] = a.l2red ? __ldcg(reinterpret_cast<const float4*>(l2base + z * zstride + row * 128))
+                                  : tc::ld_dsmem_f4(tc::map_cluster(tile_s + off, z));
       } else {
         part[rb][0] = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(tile) + off);
       }
@@ -646,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
     }
   }
   if (tid == 0) PHASE(6);
-  if (splits > 1) tc::cluster_sync();  // peers may still be reading this CTA's tile
+  if (splits > 1 && !a.l2red) tc::cluster_sync();  // peers may still be reading this CTA's tile
   PHASE_FLUSH();
     trace_end(trace);
 }
@@ -828,13 +843,20 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
   a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
             op.i[26] == 0) ? 1 : 0;
+  a.l2red = (a.splits > 1 && op.i[26] == 2) ? 1 : 0;
+  a.ws = nullptr;
   LaunchCfg c;
   c.func = func;
   c.grid = dim3(ceil_div(a.M, bn), mtiles, a.splits);
   c.block = dim3(kThreads);
   c.smem = v[id].smem + (a.push ? recv_bytes : 0);
+  c.workspace = a.l2red ? static_cast<size_t>(c.grid.x) * c.grid.y * c.grid.z * bn * 128 * 4 : 0;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
+  if (a.l2red) {
+    if (!op.p[7]) return fail(OPARA_ERR_INTERNAL, "conv2d_tc_bf16: split-K workspace missing");
+    a.ws = static_cast<float*>(op.p[7]);
+  }
   opara_status st = set_attr_once(func, attr_smem(v[id].smem));
   if (st != OPARA_OK) return st;
   if (!encode(bn)) return fail(OPARA_ERR_CUDA, "conv2d_tc_bf16: cuTensorMapEncodeIm2col failed");

@@ -14,7 +14,8 @@
 //                 1 tcgen05 3xTF32, 2 tcgen05 bf16), 23 output dtype, 24 activation
 //                 (0 none, 1 ReLU, 2 GELU, 3 tanh), 25 relu_in (ReLU fused on the input),
 //                 26 split-K reduction (0 push partials to the owner CTA when its buffer
-//                 fits, 1 pull over DSMEM after a cluster barrier)
+//                 fits, 1 pull over DSMEM after a cluster barrier, 2 partial tiles through
+//                 an L2 workspace in p[7] after a cluster barrier)
 //              p: 0 in, 1 weight: engine 0 [R*S*Cin][Cout] (k = (r*S + s)*Cin + c);
 //                 engine 1 packed tf32 hi/lo UMMA images (conv_tc.cu), 2 bias [Cout], 3 out,
 //                 7 split-K workspace (executor-owned)

@@ -204,7 +204,7 @@ def concurrency_targets(program: Program, num_sms: int = 148, scale: float = 1.0
     return out
 
 
-SPLITK_MODES = {"push": 0, "pull": 1}
+SPLITK_MODES = {"push": 0, "pull": 1, "l2": 2}
 
 
 def _op_record(op, views, weights, conv_engine: int = 1, target_ctas: int = 0,
@@ -339,11 +339,12 @@ class ScheduledGraph:
         self.bound_grids = bool(bound_grids)
         self.bound_scale = bound_scale
         # split-K reduction: "push" (partials bulk-copied to the owner CTA), "pull" (DSMEM after a
-        # cluster barrier), or "auto": pull where other convs share the DAG level
-        # (concurrent branches), push for convs that run alone
+        # cluster barrier), "l2" (partial tiles through L2 after a cluster barrier), or "auto":
+        # pull where other convs share the DAG level (concurrent branches), l2 for convs that run
+        # alone (their tiles would cross the smem ports twice in a DSMEM pull)
         self.splitk = splitk
         conc = concurrent_convs(program) if splitk == "auto" else {}
-        mode_of = {k: (SPLITK_MODES["pull"] if conc.get(k, 1) > 1 else SPLITK_MODES["push"]) if splitk == "auto"
+        mode_of = {k: (SPLITK_MODES["pull"] if conc.get(k, 1) > 1 else SPLITK_MODES["l2"]) if splitk == "auto"
                    else SPLITK_MODES[splitk] for k in range(len(program.ops))}
         self.targets = concurrency_targets(program, scale=bound_scale) if bound_grids else {}
         for k, op in enumerate(program.ops):
@@ -829,7 +830,7 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
     bound_grids: False = every conv/GEMM sized for the whole GPU; True =
     Opara's bounded grids (each conv sized for its DAG level's share of the
     SMs, so concurrent branches co-reside); "auto" = build every combination
-    of {full, bounded} grids x {push, pull, auto} split-K reductions (and,
+    of {full, bounded} grids x {push, pull, l2, auto} split-K reductions (and,
     for the fastest bounded one, SM-share scales 0.75 / 1.5 / 2), replay each Opara
     graph and keep the fastest (all latencies are kept in ``autotune``).  tune: pick every tensor-core
     conv/GEMM's tile width and split-K by measurement (ScheduledGraph._autotune).
@@ -863,7 +864,7 @@ def compile(model: torch.nn.Module, example, *, device: int = 0, policy: str = "
             sg.close()
 
     for bounded in (False, True):
-        for splitk in ("push", "pull", "auto"):
+        for splitk in ("push", "pull", "l2", "auto"):
             trial(bounded, splitk)
     # refine the SM shares of the fastest bounded variant (even when a full-grid
     # variant leads: a larger share often overtakes it)

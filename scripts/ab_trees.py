@@ -25,7 +25,7 @@ for cfg in %r:
     seq = sorted(sg.time(engine.SLOT_SEQUENTIAL, iters=200).median_ms for _ in range(3))[1]
     print("   ", cfg, "par %%.4f seq %%.4f x %%.3f" %% (par, seq, seq / par), flush=True)
 ''' % (model, dtype, configs)
-for rnd in range(2):
+for rnd in range(int(os.environ.get("AB_ROUNDS", "2"))):
     for t in trees:
         env = dict(os.environ, OPARA_TUNE_CACHE=f"/tmp/ab_tune_{os.path.basename(t.rstrip('/')) or 'head'}.json")
         print(f"round {rnd} tree {t}", flush=True)

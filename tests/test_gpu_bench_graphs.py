@@ -104,8 +104,9 @@ def test_bench_graph_parity(model, dtype, batch):
         sg.close()
 
 
-@pytest.mark.parametrize("bounded,splitk,scale", [(False, "push", 1.0), (False, "pull", 1.0), (False, "auto", 1.0),
-                                                  (True, "push", 1.0), (True, "pull", 1.0), (True, "auto", 1.0),
+@pytest.mark.parametrize("bounded,splitk,scale", [(False, "push", 1.0), (False, "pull", 1.0), (False, "l2", 1.0),
+                                                  (False, "auto", 1.0), (True, "push", 1.0), (True, "pull", 1.0),
+                                                  (True, "l2", 1.0), (True, "auto", 1.0),
                                                   (True, "pull", 0.75), (True, "pull", 1.5), (True, "pull", 2.0)])
 @pytest.mark.parametrize("model,dtype", [("inception_v3", "f32"), ("googlenet", "bf16")])
 def test_every_autotune_variant(model, dtype, bounded, splitk, scale):

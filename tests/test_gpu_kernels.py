@@ -66,7 +66,7 @@ CONV_CASES = [
 ]
 
 
-@pytest.mark.parametrize("engine_name", ["tc", "tc-pull", "simt"])
+@pytest.mark.parametrize("engine_name", ["tc", "tc-pull", "tc-l2", "simt"])
 @pytest.mark.parametrize("case", CONV_CASES, ids=[str(c) for c in CONV_CASES])
 def test_conv_matches_torch(case, engine_name):
     """Oracle: the same module in float64 on the CPU (cuDNN fp32 may pick
@@ -77,7 +77,7 @@ def test_conv_matches_torch(case, engine_name):
     m = Wrap(cin, cout, k, s, p, hw).eval()
     x = torch.randn(1, 3, hw, hw)
     sg = engine.compile(m, x, device=0, profile_reps=2, conv_engine=engine_name.split("-")[0],
-                        splitk="pull" if engine_name.endswith("pull") else None)
+                        splitk=engine_name.split("-")[1] if "-" in engine_name else None)
     y = sg.run(x.cuda())
     with torch.no_grad():
         ref = m.double()(x.double())
@@ -100,7 +100,7 @@ BF16_CASES = [
 ]
 
 
-@pytest.mark.parametrize("splitk", ["push", "pull"])
+@pytest.mark.parametrize("splitk", ["push", "pull", "l2"])
 @pytest.mark.parametrize("case", BF16_CASES, ids=[str(c) for c in BF16_CASES])
 def test_conv_bf16_matches_torch(case, splitk):
     """bf16 tcgen05 engine (kind::f16, fp32 accumulation) vs the fp64 module;

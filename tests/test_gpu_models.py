@@ -112,10 +112,10 @@ def test_nasnet_large_parity(dtype, tol):
     assert rel <= tol, rel
 
 
-@pytest.mark.parametrize("splitk", ["push", "pull", "auto"])
+@pytest.mark.parametrize("splitk", ["push", "pull", "l2", "auto"])
 def test_splitk_reductions_agree(splitk):
     """Every split-K reduction (bulk-copy push to the owner CTA, DSMEM pull after
-    a cluster barrier, per-level auto) gives
+    a cluster barrier, L2 partial tiles after a cluster barrier, per-level auto) gives
     the same network output within the bf16 tolerance, and each graph pair
     (Opara / sequential) is bit-identical."""
     from paper_2312_10351_b200 import engine, zoo
