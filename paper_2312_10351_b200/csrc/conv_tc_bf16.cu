@@ -68,7 +68,9 @@ __device__ unsigned g_phase_n;
 constexpr int kBK = 32;                     // bf16 k elements per stage (64 B rows)
 constexpr int kGatherWarps = 4;
 constexpr int kLoadWarp = 4, kMmaWarp = 5;
-constexpr int kThreads = 192;
+constexpr int kXWarp = 6;          // folded-LayerNorm consumers: issues the o + r TMA tiles
+constexpr int kMaxLnTiles = 8;     // folded LayerNorm: channels <= 1024
+constexpr int kThreads = 224;      // (a 7th warp measured neutral on the CNNs, BERT 0.440 -> 0.430 ms vs sharing a gather warp)
 constexpr int kMaxSplits = 8;
 constexpr int kPushMaxKB = 48;   // split-K push receive buffer limit (KB of smem beyond the ring)
 constexpr uint32_t kWBytes = 128 * kBK * 2;  // 8 KB
@@ -78,8 +80,8 @@ constexpr uint32_t kWBytes = 128 * kBK * 2;  // 8 KB
 // before griddepcontrol.wait (weights do not depend on the predecessor), so
 // after the wait only the small activation tile is on the critical path.
 __host__ __device__ constexpr int bf_stages(int bn) { return bn == 16 ? 24 : bn <= 64 ? 8 : 6; }
-// full[], empty[], accum, tmem slot, push barrier: rounded up to 128 bytes
-__host__ __device__ constexpr int bf_bar_bytes(int stages) { return ((2 * stages + 3) * 8 + 127) / 128 * 128; }
+// full[], empty[], accum, tmem slot, push barrier, landed[]: rounded up to 128 bytes
+__host__ __device__ constexpr int bf_bar_bytes(int stages) { return ((3 * stages + 3) * 8 + 127) / 128 * 128; }
 
 // kVecBf16: 16-byte cp.async of 8 channels (Cin % 8 == 0); kSub4 / kSub2: each
 // 16-byte smem chunk assembled from 8- / 4-byte cp.asyncs of 4 / 2 channels
@@ -99,6 +101,7 @@ __device__ __forceinline__ void cp_async_sub(uint32_t dst, const void* src, int 
 
 struct BfArgs {
   CUtensorMap tmap;                         // im2col map of the input view (kTma only)
+  CUtensorMap tmap_r;                       // map of the LayerNorm residual view (ln_in only)
   const void* in;
   const __nv_bfloat16* __restrict__ wpack;  // [m_tiles][kblocks][atom][row][chunk][8]
   const float* __restrict__ bias;
@@ -114,6 +117,23 @@ struct BfArgs {
   float* ws;
   const int4* ktab;     // scalar gathers: per k (dr, dq, input offset) from the host (no divisions)
   int64_t sN, sH, sW, sC;
+  // Folded LayerNorm y = LN(o + r) (frontend.PendingLN).  Producer GEMM
+  // (res_stats): stores o = bf16(acc + bias) as usual and, per token, the sum
+  // and sum of squares of o + r (fp32, r = the bf16 residual view) over this
+  // CTA's 128 channels into stats_out[token][m-tile][2].  Consumer GEMM
+  // (ln_in): the X warp lands the o and r tiles of every stage; the gather
+  // warps form (o + r - mean) * rstd * gamma + beta in place (the same
+  // roundings as the unfolded LayerNorm kernel) before the MMA reads it; lnout
+  // (first consumer, m-tile 0 CTAs) receives the normalised rows.
+  int res_stats, res_cs;
+  const __nv_bfloat16* res;
+  float* stats_out;
+  int ln_in, ln_tiles, lnout_cs;
+  const float* stats_in;
+  const float* gb;          // [2][Cin]: gamma, beta
+  __nv_bfloat16* lnout;
+  float eps;
+  uint32_t r_off;           // smem byte offset of the residual tiles (kStages x BN x 64 B), then mean / rstd [BN]
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
@@ -177,13 +197,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
   // push-mode split-K: receive buffer [src rank][128 channels][rows_per columns]
   // fp32 behind the ring (other CTAs may push while this CTA's ring is busy)
   uint64_t* rbar = accum + 2;
+  uint64_t* landed = rbar + 1;   // TMA tile landed (folded-LayerNorm consumers: normalised before full[])
   float* recv = reinterpret_cast<float*>(smem + kStages * kStage + bf_bar_bytes(kStages));
   const bool push = a.push != 0;
+  const bool ln_in = kMode == kTma && a.ln_in;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      // gather threads (or the TMA thread's expect_tx arrive) + the weight loader
-      tc::mbar_init(&full[s], kMode == kTma ? 2 : 32 * kGatherWarps + 1);
+      // gather threads (or the TMA thread's expect_tx arrive, or the normalising
+      // threads after it) + the weight loader
+      tc::mbar_init(&full[s], kMode == kTma ? (ln_in ? 32 + 1 : 2) : 32 * kGatherWarps + 1);
       tc::mbar_init(&empty[s], 1);
+      if (ln_in) tc::mbar_init(&landed[s], 1);
     }
     tc::mbar_init(accum, 1);
     if (push) tc::mbar_init(rbar, 1);
@@ -257,7 +281,74 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
     if constexpr (kMode == kTma) {
       // k = (r*S + s)*Cin + c with Cin % 32 == 0: every stage is one tap's
       // 32-channel slice of BN output pixels; padding and the tile tail are zeros
-      if (tid == 0) {
+      if (ln_in) {
+        // Folded LayerNorm on load (1x1 row GEMMs: k = channel).  The X warp
+        // lands each stage's o and r tiles on landed[]; gather warp w
+        // normalises whole stages i = w (mod 4) in place — four stages in
+        // flight, one warp each — and releases full[].  Lane l owns chunk
+        // l % 4 (8 channels) of rows l / 4, l / 4 + 8, ...  Per-token mean and
+        // rstd (from the producer's partial sums, summed in m-tile order) are
+        // computed once into smem (behind the residual tiles).
+        float* ln_mean = reinterpret_cast<float*>(smem + a.r_off + kStages * kXBytes);
+        float* ln_rstd = ln_mean + BN;
+        for (int row = tid; row < BN; row += 32 * kGatherWarps) {
+          const int p = n0 + row;
+          float s1 = 0.f, s2 = 0.f;
+          if (p < a.M) {
+            const float2* st = reinterpret_cast<const float2*>(a.stats_in) + static_cast<int64_t>(p) * a.ln_tiles;
+            float2 v[kMaxLnTiles];   // every partial's load in flight
+#pragma unroll
+            for (int t = 0; t < kMaxLnTiles; ++t)
+              if (t < a.ln_tiles) v[t] = __ldcg(st + t);
+#pragma unroll
+            for (int t = 0; t < kMaxLnTiles; ++t)
+              if (t < a.ln_tiles) {
+                s1 += v[t].x;
+                s2 += v[t].y;
+              }
+          }
+          const float mu = s1 / a.Cin;
+          ln_mean[row] = mu;
+          ln_rstd[row] = rsqrtf(fmaxf(s2 / a.Cin - mu * mu, 0.f) + a.eps);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kGatherWarps) : "memory");   // the gather warps only
+        const int c4 = lane & 3, rl = lane >> 2;
+        const bool write = a.lnout && mt == 0;
+        for (int i = rw; i < nkb; i += kGatherWarps) {
+          const int s = i % kStages;
+          const int c0 = (kb0 + i) * kBK + c4 * 8;   // this lane's 8 channels
+          const float4* g4 = reinterpret_cast<const float4*>(a.gb + c0);
+          const float4* b4 = reinterpret_cast<const float4*>(a.gb + a.Cin + c0);
+          const float4 ga = __ldg(g4), gb2 = __ldg(g4 + 1), ba = __ldg(b4), bb = __ldg(b4 + 1);
+          const float g[8] = {ga.x, ga.y, ga.z, ga.w, gb2.x, gb2.y, gb2.z, gb2.w};
+          const float b[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+          tc::mbar_wait(&landed[s], (i / kStages) & 1);
+          uint8_t* xs = smem + s * kStage + kWBytes;
+          const uint8_t* rs = smem + a.r_off + s * kXBytes;
+#pragma unroll 4
+          for (int row = rl; row < BN; row += 8) {
+            const int r8 = row & 7;
+            const uint32_t off = static_cast<uint32_t>(row >> 3) * kSbo + r8 * 64u +
+                                 static_cast<uint32_t>((c4 ^ ((r8 >> 1) & 3)) * 16);
+            uint4 v = *reinterpret_cast<const uint4*>(xs + off);
+            const uint4 rv = *reinterpret_cast<const uint4*>(rs + off);
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+            const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+            const float mu = ln_mean[row], rsd = ln_rstd[row];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h2[e]), fr = __bfloat1622float2(r2[e]);
+              h2[e] = __floats2bfloat162_rn((f.x + fr.x - mu) * rsd * g[2 * e] + b[2 * e],
+                                            (f.y + fr.y - mu) * rsd * g[2 * e + 1] + b[2 * e + 1]);
+            }
+            *reinterpret_cast<uint4*>(xs + off) = v;
+            if (write && n0 + row < a.M)
+              *reinterpret_cast<uint4*>(a.lnout + static_cast<int64_t>(n0 + row) * a.lnout_cs + c0) = v;
+          }
+          tc::fence_proxy_async_smem();
+          tc::mbar_arrive(&full[s]);
+        }
+      } else if (tid == 0) {
         const int ohw = a.OH * a.OW;
         const int b = n0 / ohw, rem = n0 - b * ohw, oh = rem / a.OW, ow = rem - oh * a.OW;
         const int w0 = ow * a.sw - a.pw, h0 = oh * a.sh - a.ph;
@@ -433,6 +524,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
         tc::mbar_arrive(&full[s]);
       }
     }
+  } else if (warp == kXWarp) {
+    if (ln_in && lane == 0) {
+      // folded-LayerNorm consumers: each stage's o and r tiles land on
+      // landed[]; the gather warps normalise them before releasing full[]
+      pdl_wait();
+      const int kc = kb0 * kBK;
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&landed[s], 2 * kXBytes);
+        tc::tma_im2col_4d(smem + s * kStage + kWBytes, &a.tmap, kc + i * kBK, n0, 0, 0, 0, 0, &landed[s]);
+        tc::tma_im2col_4d(smem + a.r_off + s * kXBytes, &a.tmap_r, kc + i * kBK, n0, 0, 0, 0, 0, &landed[s]);
+      }
+    }
   } else if (warp == kLoadWarp) {
     if (lane == 0) {
       // ring refills beyond the first kStages come from L2: request the rest of
@@ -449,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
         tc::bulk_g2s(smem + s * kStage, src, kWBytes, &full[s]);
       }
     }
-  } else if (lane == 0) {
+  } else if (warp == kMmaWarp && lane == 0) {
     for (int i = 0; i < nkb; ++i) {
       const int s = i % kStages;
       tc::mbar_wait(&full[s], (i / kStages) & 1);
@@ -634,6 +739,29 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
         }
       float y[4] = {act_fn(acc.x + bias[0], a.act), act_fn(acc.y + bias[1], a.act),
                     act_fn(acc.z + bias[2], a.act), act_fn(acc.w + bias[3], a.act)};
+      if (a.res_stats) {
+        // folded LayerNorm producer: the warp holds this token's 128 channels of
+        // the m-tile; the sum and sum of squares of o + r (fixed xor-tree order)
+        // go to stats_out[token][m-tile]
+        const uint2 rr = *reinterpret_cast<const uint2*>(a.res + static_cast<int64_t>(p) * a.res_cs + ch);
+        const float2 r01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rr.x));
+        const float2 r23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rr.y));
+        const float r[4] = {r01.x, r01.y, r23.x, r23.y};
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {   // the consumer normalises bf16(o) + r: the same values
+          const float u = __bfloat162float(__float2bfloat16_rn(y[e])) + r[e];
+          s1 += u;
+          s2 += u * u;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (lane == 0)
+          reinterpret_cast<float2*>(a.stats_out)[static_cast<int64_t>(p) * gridDim.y + mt] = make_float2(s1, s2);
+      }
       TO* dst = out + static_cast<int64_t>(p) * a.out_cs + a.out_coff + ch;
       if constexpr (std::is_same<TO, float>::value) {
         if (a.vec_out && ch + 3 < a.Cout) {
@@ -804,6 +932,23 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   const BfVariant* v = bf_variants();
   const int mtiles = (a.Cout + 127) / 128;
   a.ktab = static_cast<const int4*>(op.p[5]);
+  a.res_stats = static_cast<int>(op.i[27]);
+  a.res_cs = static_cast<int>(op.i[28]);
+  a.res = a.res_stats ? static_cast<const __nv_bfloat16*>(op.p[4]) : nullptr;
+  a.stats_out = a.res_stats ? static_cast<float*>(op.p[6]) : nullptr;
+  a.ln_in = static_cast<int>(op.i[29]);
+  a.lnout_cs = static_cast<int>(op.i[30]);
+  a.ln_tiles = static_cast<int>(op.i[31]);
+  a.stats_in = a.ln_in ? static_cast<const float*>(op.p[4]) : nullptr;
+  a.gb = a.ln_in ? static_cast<const float*>(op.p[5]) : nullptr;
+  a.lnout = a.ln_in ? static_cast<__nv_bfloat16*>(op.p[6]) : nullptr;
+  a.eps = static_cast<float>(op.f[0]);
+  if (a.res_stats && a.ln_in) return fail(OPARA_ERR_VALUE, "conv2d_tc_bf16: one folded LayerNorm role per GEMM");
+  if (a.res_stats && (a.Cout % 128 || a.act != 0 || out_f32 || a.res_cs % 4))
+    return fail(OPARA_ERR_VALUE, "conv2d_tc_bf16: residual + stats epilogue needs whole 128-channel tiles, "
+                                 "no activation, bf16 output");
+  if (a.ln_in && (mode != kTma || a.R != 1 || a.S != 1 || a.Cin % 128 || (a.lnout && a.lnout_cs % 8)))
+    return fail(OPARA_ERR_VALUE, "conv2d_tc_bf16: LayerNorm on load needs a TMA-eligible 1x1 row GEMM");
   int id = op.variant;
   if (id < 0 || id > 4) {   // 0..3: tile width 32 << id, 4: width 16 (deep weight ring)
     id = 0;
@@ -829,7 +974,8 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
     while (splits > 1) {
       const int rp = ((bn + static_cast<int>(splits) - 1) / static_cast<int>(splits) + 3) / 4 * 4;
       const size_t rb = static_cast<size_t>(splits) * 128 * rp * 4;
-      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && op.i[26] == 0;
+      const bool pu = rb <= kPushMaxBytes && v[id].smem + rb <= kSmemLimit && op.i[26] == 0 && !a.res_stats &&
+                      !a.ln_in;
       const size_t sm = v[id].smem + (pu ? rb : 0);
       if (base <= max_clusters(func, static_cast<int>(splits), sm, attr_smem(v[id].smem))) break;
       --splits;
@@ -841,15 +987,24 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   // small; otherwise pull over DSMEM after a cluster barrier.
   a.rows_per = ((bn + a.splits - 1) / a.splits + 3) / 4 * 4;
   const size_t recv_bytes = static_cast<size_t>(a.splits) * 128 * a.rows_per * 4;
+  // (the residual + stats epilogue lives in the pull / L2 reduction loop, and
+  // LayerNorm-on-load consumers keep their residual tiles where push receives)
+  const bool folded = a.res_stats || a.ln_in;
   a.push = (a.splits > 1 && recv_bytes <= kPushMaxBytes && v[id].smem + recv_bytes <= kSmemLimit &&
-            op.i[26] == 0) ? 1 : 0;
-  a.l2red = (a.splits > 1 && op.i[26] == 2) ? 1 : 0;
+            op.i[26] == 0 && !folded) ? 1 : 0;
+  a.l2red = (a.splits > 1 && (op.i[26] == 2 || (op.i[26] == 0 && folded))) ? 1 : 0;
+  // LayerNorm-on-load: the residual tiles (kStages x BN x 64 B) behind the ring and barriers
+  const size_t ring = static_cast<size_t>(bf_stages(bn)) * (kWBytes + static_cast<size_t>(bn) * kBK * 2);
+  a.r_off = static_cast<uint32_t>((ring + bf_bar_bytes(bf_stages(bn)) + 1023) / 1024 * 1024);
+  const size_t r_bytes = a.ln_in ? static_cast<size_t>(bf_stages(bn)) * bn * kBK * 2 + 2 * bn * 4 + 1024 : 0;
+  if (a.ln_in && v[id].smem + r_bytes > std::min(attr_smem(v[id].smem), kSmemLimit))
+    return fail(OPARA_ERR_VALUE, "conv2d_tc_bf16: LayerNorm on load: residual tiles do not fit this tile width");
   a.ws = nullptr;
   LaunchCfg c;
   c.func = func;
   c.grid = dim3(ceil_div(a.M, bn), mtiles, a.splits);
   c.block = dim3(kThreads);
-  c.smem = v[id].smem + (a.push ? recv_bytes : 0);
+  c.smem = v[id].smem + (a.push ? recv_bytes : 0) + r_bytes;
   c.workspace = a.l2red ? static_cast<size_t>(c.grid.x) * c.grid.y * c.grid.z * bn * 128 * 4 : 0;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
@@ -860,6 +1015,12 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   opara_status st = set_attr_once(func, attr_smem(v[id].smem));
   if (st != OPARA_OK) return st;
   if (!encode(bn)) return fail(OPARA_ERR_CUDA, "conv2d_tc_bf16: cuTensorMapEncodeIm2col failed");
+  if (a.ln_in) {   // the residual view r of LN(o + r): i[32] address, i[33] cstride (same [T][C] shape)
+    const void* rbase = reinterpret_cast<const void*>(static_cast<uintptr_t>(op.i[32]));
+    if (!rbase || !make_im2col_map(&a.tmap_r, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rbase, a.N, a.H, a.W, a.Cin,
+                                   op.i[33], 0, a.OH, a.OW, a.sh, a.sw, a.ph, a.pw, kBK, bn))
+      return fail(OPARA_ERR_CUDA, "conv2d_tc_bf16: LayerNorm residual tensor map");
+  }
   void* args[] = {&a, &trace};
   return launch_kernel(c, args, s, a.splits > 1 ? static_cast<unsigned>(a.splits) : 1u);
 }

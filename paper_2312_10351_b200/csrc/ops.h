@@ -15,7 +15,12 @@
 //                 (0 none, 1 ReLU, 2 GELU, 3 tanh), 25 relu_in (ReLU fused on the input),
 //                 26 split-K reduction (0 push partials to the owner CTA when its buffer
 //                 fits, 1 pull over DSMEM after a cluster barrier, 2 partial tiles through
-//                 an L2 workspace in p[7] after a cluster barrier)
+//                 an L2 workspace in p[7] after a cluster barrier),
+//                 folded LayerNorm y = LN(o + r) (bf16 engine, conv_tc_bf16.cu BfArgs):
+//                 27 producer epilogue (p[4] residual r view, i[28] its cstride, p[6] stats
+//                 [T][Cout/128][2] of o + r), 29 LayerNorm on load (p[4] stats, i[31] stats
+//                 tiles, p[5] gamma|beta fp32 [2][Cin], f[0] eps, i[32] r view address,
+//                 i[33] its cstride, p[6] + i[30] normalised-rows view written, or null)
 //              p: 0 in, 1 weight: engine 0 [R*S*Cin][Cout] (k = (r*S + s)*Cin + c);
 //                 engine 1 packed tf32 hi/lo UMMA images (conv_tc.cu), 2 bias [Cout], 3 out,
 //                 7 split-K workspace (executor-owned)

@@ -32,7 +32,8 @@ from . import _lib
 from .dag import ComputationGraph, OpClass, OperatorNode, ResourceDemand, graph_to_dict
 from .device import GpuConfig, device_gpu_config, GPU_PRESETS
 from .frontend import (ADD, ATTENTION, AVGPOOL2D, CONV2D, COPY, DWCONV2D, EMBEDDING, FIELD_EMBEDDING, FIRST_ORDER,
-                       FM, GLOBAL_AVGPOOL, LAYERNORM, LINEAR, MAXPOOL2D, NOP, PACK_INPUT, RELU, Program, lower)
+                       FM, GLOBAL_AVGPOOL, LAYERNORM, LINEAR, MAXPOOL2D, NOP, PACK_INPUT, RELU, LoweringError,
+                       Program, lower)
 from .order import LaunchSchedule, make_order
 from .plan import StreamPlan, allocate_streams, plan_to_dict, single_stream_plan
 
@@ -358,6 +359,8 @@ class ScheduledGraph:
                     ktab = self._gather_table(op)
                     if ktab is not None:
                         recs[k].p[5] = ktab
+                if op.kind == CONV2D and (op.ints.get("res_stats") or op.ints.get("ln_in")):
+                    self._fold_ln_record(op, recs[k])
         self.debug_ts = {}
         if os.environ.get("OPARA_CONV_DEBUG"):  # per-phase timestamps of CTA 0 (conv_tc.cu)
             for k, op in enumerate(program.ops):
@@ -428,6 +431,33 @@ class ScheduledGraph:
         out.append((self._bufs[r.tid].data_ptr(), off, r.shape[-1]))
         return out
 
+    def _buf_view(self, t, esize):
+        """(device address of t's first element, cstride) of a channel view."""
+        r, off = t.root()
+        return self._bufs[r.tid].data_ptr() + esize * off, r.shape[-1]
+
+    def _fold_ln_record(self, op, rec) -> None:
+        """Folded LayerNorm (frontend.PendingLN) on the bf16 engine
+        (conv_tc_bf16.cu): i[27] residual + stats epilogue (p[4] residual view,
+        i[28] its cstride, p[6] stats [T][tiles][2]); i[29] LayerNorm of the A
+        tiles on load (p[4] stats, p[5] gamma|beta, f[0] eps, i[31] stats tiles,
+        i[32] + i[33] the residual view r of LN(o + r), p[6] + i[30] the
+        normalised-rows view this GEMM writes, or null)."""
+        if rec.i[22] != 2:
+            raise LoweringError(f"{op.label}: a folded LayerNorm needs the bf16 tensor-core engine")
+        if op.ints.get("res_stats"):
+            rec.i[27] = 1
+            rec.p[4], rec.i[28] = self._buf_view(op.inputs[1], 2)
+            rec.p[6] = self._buf_view(op.extra_outputs[0], 4)[0]
+        if op.ints.get("ln_in"):
+            rec.i[29], rec.i[31] = 1, op.ints["ln_tiles"]
+            rec.p[4] = self._buf_view(op.inputs[1], 4)[0]
+            rec.p[5] = self._arrays(op)["gb"]
+            rec.f[0] = op.floats[0]
+            rec.i[32], rec.i[33] = self._buf_view(op.inputs[2], 2)
+            if op.ints.get("ln_write"):
+                rec.p[6], rec.i[30] = self._buf_view(op.extra_outputs[0], 2)
+
     def _arrays(self, op):
         ptrs = {}
         for name, arr in op.arrays.items():
@@ -482,7 +512,7 @@ class ScheduledGraph:
     def _tune_key(rec) -> tuple:
         """Launch-shape signature of a tensor-core conv record (no pointers)."""
         return (rec.i[22],) + tuple(rec.i[k] for k in (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15,
-                                                       16, 17, 18, 20, 23, 24, 25, 26))
+                                                       16, 17, 18, 20, 23, 24, 25, 26, 27, 29, 30))
 
     def _autotune(self, recs) -> dict:
         """Pick each tensor-core conv/GEMM's tile width and split-K by

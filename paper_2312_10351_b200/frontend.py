@@ -77,6 +77,26 @@ class LoweredOp:
     label: str = ""           # fx node name, for reports
     arrays: dict = field(default_factory=dict)  # extra host arrays (tables, LN affine)
     floats: tuple = ()        # float parameters (eps, scale)
+    extra_outputs: list = field(default_factory=list)   # further tensors this op writes
+
+
+@dataclass
+class PendingLN:
+    """add_layer_norm(o, res) folded into the GEMMs around it (bf16 rows path):
+    the GEMM producing `o` also stores, per (token, 128-channel tile), the sum
+    and sum of squares of o + res into `stats`; every consuming GEMM loads the
+    o and res tiles and normalises o + res on load from those sums and gamma /
+    beta (the unfolded kernel's roundings), and the first one also stores the
+    normalised rows into `out`, which later add_layer_norms read as their
+    residual.  No LayerNorm kernel is launched."""
+
+    o: Tensor
+    res: Tensor
+    stats: Tensor
+    gb: np.ndarray            # [2][C] fp32: gamma, beta
+    eps: float
+    out: Tensor
+    writer: int | None = None
 
 
 class LoweringError(RuntimeError):
@@ -136,9 +156,10 @@ def _fold_bn(conv: nn.Conv2d, bn: nn.BatchNorm2d | None):
 
 
 class _Lowerer:
-    def __init__(self, gm: fx.GraphModule, dtype: str = "f32"):
+    def __init__(self, gm: fx.GraphModule, dtype: str = "f32", fold_ln: bool = True):
         self.gm = gm
         self.act_dtype = dtype          # element type of conv / pool activations
+        self.fold_ln = fold_ln          # fold add_layer_norm into the GEMMs around it (bf16)
         self.esize = 2 if dtype == "bf16" else 4
         self.ops: list[LoweredOp] = []
         self.tensors: list[Tensor] = []
@@ -157,6 +178,8 @@ class _Lowerer:
         idx = len(self.ops)
         self.ops.append(op)
         op.output.producers = {idx}
+        for t in op.extra_outputs:
+            t.producers = {idx}
 
     @staticmethod
     def _esz(t: Tensor) -> int:
@@ -166,8 +189,13 @@ class _Lowerer:
 
     def value(self, arg) -> Tensor:
         """The materialised tensor of an fx argument: a pending ReLU is
-        launched once as a RELU op (the unfused fallback) and cached."""
+        launched once as a RELU op (the unfused fallback) and cached; a folded
+        LayerNorm is its normalised rows (written by its first consuming GEMM)."""
         v = self.env[arg]
+        if isinstance(v, PendingLN):
+            if v.writer is None:
+                raise LoweringError(f"{arg}: folded LayerNorm read before a consuming GEMM wrote it")
+            return v.out
         if not isinstance(v, Lazy):
             return v
         if v.sub is not None:
@@ -496,7 +524,9 @@ class _Lowerer:
         return obj.detach().float().cpu()
 
     def lower_linear_rows(self, node):
-        x = self.value(node.args[0])
+        pend = self.env[node.args[0]]
+        pend = pend if isinstance(pend, PendingLN) else None
+        x = pend.o if pend is not None else self.value(node.args[0])
         w = self._param(node.args[1])
         b = self._param(node.args[2]) if len(node.args) > 2 and node.args[2] is not None else None
         n, h, t, k = x.shape
@@ -519,6 +549,19 @@ class _Lowerer:
         op = LoweredOp(CONV2D, "gemm", OpClass.COMPUTE, ints, [x], out, w.t().contiguous().numpy(), bias,
                        flops=2 * t * k * nout, bytes_min=self.esize * (t * k + k * nout + t * nout) + 4 * nout,
                        label=node.name)
+        if pend is not None:
+            # LayerNorm of the activation rows on load (stats from the producing GEMM)
+            ints.update(ln_in=1, ln_tiles=k // 128)
+            op.inputs += [pend.stats, pend.res]
+            op.arrays = {"gb": pend.gb}
+            op.floats = (pend.eps,)
+            op.flops += 4 * t * k
+            op.bytes_min += 4 * pend.stats.shape[0] * pend.stats.shape[1] + 8 * k + self.esize * t * k
+            if pend.writer is None:   # the first consumer materialises the normalised rows
+                ints["ln_write"] = 1
+                op.extra_outputs.append(pend.out)
+                op.bytes_min += self.esize * t * k
+                pend.writer = len(self.ops)
         self.emit(op)
         self.env[tail] = out
 
@@ -546,7 +589,49 @@ class _Lowerer:
         self.emit(op)
         self.env[node] = out
 
+    def _ln_foldable(self, node) -> bool:
+        """add_layer_norm(o, res) folds into GEMMs when o comes from a bf16 row
+        GEMM without activation used only here, every user is a linear layer
+        reading it (at least one, lowered before any residual user) or a later
+        add_layer_norm reading it as its residual, and C is whole 128-channel
+        tiles.  The model's output LayerNorm (read by first_token / returned)
+        stays a kernel."""
+        if self.act_dtype != "bf16" or not self.fold_ln:
+            return False
+        o = node.args[0]
+        ot = self.env.get(o)
+        if not isinstance(ot, Tensor) or len(o.users) != 1 or not ot.producers or ot.alias is not None:
+            return False
+        prod = self.ops[min(ot.producers)]
+        if (prod.kind != CONV2D or prod.name != "gemm" or prod.ints.get("act", 0) != 0 or prod.ints.get("ln_in")
+                or ot.shape[-1] % 128 or ot.dtype != "bf16"):
+            return False
+        order = {n: i for i, n in enumerate(self.gm.graph.nodes)}
+        lin = [u for u in node.users if u.op == "call_function" and u.target is F.linear and u.args[0] is node]
+        res = [u for u in node.users if u.op == "call_function" and getattr(u.target, "__name__", "") ==
+               "add_layer_norm" and u.args[1] is node and u.args[0] is not node]
+        if not lin or len(lin) + len(res) != len(node.users):
+            return False
+        first = min(order[u] for u in lin)
+        return all(order[u] > first for u in res)
+
     def lower_add_layernorm(self, node):
+        if self._ln_foldable(node):
+            o = self.env[node.args[0]]
+            pidx = min(o.producers)
+            prod = self.ops[pidx]
+            r = self.value(node.args[1])
+            t, c = o.shape[2], o.shape[3]
+            stats = self.new_tensor((t, (c // 128) * 2), dtype="f32")
+            stats.producers = {pidx}
+            prod.inputs.append(r)
+            prod.extra_outputs.append(stats)
+            prod.ints["res_stats"] = 1
+            prod.flops += 3 * t * c
+            prod.bytes_min += self.esize * t * c + 4 * t * (c // 128) * 2   # residual read, stats written
+            gb = np.stack([self._param(node.args[2]).numpy(), self._param(node.args[3]).numpy()]).astype(np.float32)
+            self.env[node] = PendingLN(o, r, stats, gb, float(node.args[4]), self.new_tensor((1, 1, t, c)))
+            return
         x, r = self.value(node.args[0]), self.value(node.args[1])
         gamma, beta = self._param(node.args[2]), self._param(node.args[3])
         eps = float(node.args[4])
@@ -739,16 +824,17 @@ class _Lowerer:
         return Program(self.ops, self.tensors, inputs[0], outs[0], sorted(edges), outs, inputs)
 
 
-def lower(model: nn.Module, example, dtype: str = "f32") -> Program:
+def lower(model: nn.Module, example, dtype: str = "f32", fold_ln: bool = True) -> Program:
     """Trace `model` with torch.fx and lower it to executor operators.
 
     `example` is one input tensor or a tuple of them (one per forward
     argument).  dtype "f32": fp32 activations end to end (3xTF32 tensor-core
     convs).  dtype "bf16": bf16 activations and weights with fp32
     accumulation; the graph input stays fp32 NCHW and the classifier head
-    stays fp32."""
+    stays fp32.  fold_ln: bf16 add_layer_norm(o, res) whose users are GEMMs
+    launches no kernel (PendingLN)."""
     if dtype not in ("f32", "bf16"):
         raise ValueError(f"unknown dtype {dtype!r}")
     model = model.eval()
     gm = fx.symbolic_trace(model)
-    return _Lowerer(gm, dtype).run(example)
+    return _Lowerer(gm, dtype, fold_ln).run(example)

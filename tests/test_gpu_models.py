@@ -96,6 +96,38 @@ def test_bert_base_bf16_parity():
     assert _rel(pooled.float().reshape(ref_p.shape), ref_p) < 1e-2
 
 
+@pytest.mark.parametrize("splitk", ["pull", "l2", "push"])
+def test_bert_folded_layernorm(splitk):
+    """The 23 add_layer_norms between GEMMs launch no kernel: the producing
+    GEMM stores u = o + residual and per-(token, 128-channel tile) sums, the
+    consuming GEMMs normalise their activation tiles on load (the first one
+    writes the normalised rows for the next residual).  Same outputs as the
+    unfolded graph within the bf16 tolerance, and vs HF within 1e-2; the
+    producer's epilogue runs in the pull / L2 reduction loop whatever the
+    requested split-K mode."""
+    from paper_2312_10351_b200 import engine, frontend, zoo
+    model, ref_model, ids = zoo.build_bert()
+    with torch.no_grad():
+        ref_h, ref_p = ref_model.cuda()(ids.cuda())
+    outs = {}
+    for fold in (True, False):
+        prog = frontend.lower(model, ids, "bf16", fold_ln=fold)
+        n_ln = sum(1 for o in prog.ops if o.kind == frontend.LAYERNORM)
+        assert n_ln == (1 if fold else 24)
+        sg = engine.ScheduledGraph(prog, 0, profile_reps=2, bound_grids=True, splitk=splitk)
+        try:
+            hidden, pooled = sg.run(ids.cuda())
+            h_seq, p_seq = sg.run(ids.cuda(), slot=engine.SLOT_SEQUENTIAL)
+            assert torch.equal(hidden, h_seq) and torch.equal(pooled, p_seq)
+            outs[fold] = (hidden.float().clone(), pooled.float().clone())
+        finally:
+            sg.close()
+    for fold, (h, p) in outs.items():
+        assert _rel(h.reshape(ref_h.shape), ref_h) < 1e-2, fold
+        assert _rel(p.reshape(ref_p.shape), ref_p) < 1e-2, fold
+    assert _rel(outs[True][0], outs[False][0]) < 1e-2
+
+
 @pytest.mark.parametrize("dtype,tol", [("f32", 1e-4), ("bf16", 1e-2)])
 def test_nasnet_large_parity(dtype, tol):
     """NASNet-A Large 331x331 (~700 kernels, ~160 plan streams) through the

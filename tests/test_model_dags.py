@@ -144,7 +144,7 @@ def _workload(name):
     return m, x, "f32"
 
 
-@pytest.mark.parametrize("name,v,e,streams", [("nasnet_large", 697, 912, 159), ("bert_base", 110, 157, 25),
+@pytest.mark.parametrize("name,v,e,streams", [("nasnet_large", 697, 912, 159), ("bert_base", 87, 168, 25),
                                               ("deepfm", 36, 36, 29), ("deepfm_b32", 36, 36, 29)])
 def test_new_config_dags_match_fixture(name, v, e, streams):
     """NASNet-A Large, BERT-base and DeepFM lower to exactly the DAG the
