@@ -148,6 +148,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(const __grid_con
   const bool dbg = a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
 #define DBG(slot) \
   if (dbg) a.dbg[warp * 8 + (slot)] = global_ns();
+  // split-K rank skew: every rank of cluster (0, 0) stamps accumulator ready /
+  // partial drained / after the cluster barrier at dbg[2048 + 4 z + k]
+#define RSTAMP(k) \
+  if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) a.dbg[2048 + 4 * blockIdx.z + (k)] = global_ns();
   DBG(0);
   const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   if (a.dbg && tid == 0 && cta_lin < 96) a.dbg[64 + 2 * cta_lin] = global_ns();
@@ -495,11 +499,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(const __grid_con
       DBG(4);
       const int quarter = warp & 3, half = warp >> 2;
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+      RSTAMP(0);
       float* mine = a.ws + (static_cast<int64_t>(blockIdx.z) * tiles + tile_id) * plane + quarter * 32 + lane;
       drain_accumulators<BN, kAcc>(trow, half, [&](int col, float val) { __stcg(mine + col * 128, val); });
+      RSTAMP(1);
     }
     tc::tc_fence_before();
     tc::cluster_sync();
+    RSTAMP(2);
     if (warp == kMmaWarp) {
       tc::tc_fence_after();
       tc::tmem_dealloc(tmem, kTmemCols);
@@ -551,8 +558,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(const __grid_con
     DBG(4);
     const int quarter = warp & 3, half = warp >> 2;
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    RSTAMP(0);
     drain_accumulators<BN, kAcc>(trow, half,
                                  [&](int col, float val) { tile[col * 128 + quarter * 32 + lane] = val; });
+    RSTAMP(1);
   }
   tc::tc_fence_before();
   const int splits = a.splits;
@@ -560,6 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(const __grid_con
     tc::cluster_sync();
   else
     __syncthreads();
+  RSTAMP(2);
   // every TMEM read is done (the tile is in smem): free the columns now so a
   // PDL-launched successor CTA on this SM can allocate while we reduce
   if (warp == kMmaWarp) {
@@ -611,6 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(const __grid_con
   DBG(7);
   if (a.dbg && tid == 0 && cta_lin < 96) a.dbg[64 + 2 * cta_lin + 1] = global_ns();
 #undef DBG
+#undef RSTAMP
   trace_end(trace);
 }
 

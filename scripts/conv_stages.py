@@ -91,3 +91,17 @@ for k, buf in sorted(sg.debug_ts.items()):
         print(f"{k:4d} {(min(ent) - pe) / 1e3:7.2f} {(d[1] - pe) / 1e3:7.2f} {(d[768] - pe) / 1e3:7.2f} "
               f"{(d[256] - pe) / 1e3:7.2f}   last-CTA exit spread {(max(ext) - min(ext)) / 1e3:6.2f}")
     prev = (k, max(ext) if ext else d[0])
+
+# split-K rank skew inside cluster (0, 0): accumulator ready / partial drained /
+# past the cluster barrier, per rank, relative to the earliest rank's accumulator
+print("\nrank skew (us, cluster (0,0)): op splits | accum-ready spread | drain (rank max) | barrier exit - last accum")
+for k, buf in sorted(sg.debug_ts.items()):
+    d = buf.cpu().numpy().astype(np.int64)
+    if sg.engines.get(k) != 1 or d[0] == 0:
+        continue
+    st = [(d[2048 + 4 * z], d[2049 + 4 * z], d[2050 + 4 * z]) for z in range(8) if d[2048 + 4 * z]]
+    if len(st) < 2:
+        continue
+    acc = [t[0] for t in st]
+    print(f"{k:4d} {len(st):2d} | {(max(acc) - min(acc)) / 1e3:6.2f} | {max(t[1] - t[0] for t in st) / 1e3:6.2f} | "
+          f"{(max(t[2] for t in st) - max(acc)) / 1e3:6.2f}")
