@@ -220,6 +220,8 @@ typedef struct opara_op_profile {
   int64_t shared_mem_per_block;    /* static + dynamic bytes */
   int64_t registers_per_thread;
   double isolated_us;              /* median of in-stream event timings */
+  int64_t tmem_columns;            /* TMEM columns one block allocates (0: none) */
+  int64_t cluster_size;            /* thread-block cluster size (1: no cluster) */
 } opara_op_profile;
 
 typedef struct opara_exec opara_exec;

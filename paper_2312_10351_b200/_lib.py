@@ -62,7 +62,7 @@ class OparaOp(C.Structure):
 class OparaOpProfile(C.Structure):
     _fields_ = [("num_blocks", C.c_int64), ("threads_per_block", C.c_int64),
                 ("shared_mem_per_block", C.c_int64), ("registers_per_thread", C.c_int64),
-                ("isolated_us", C.c_double)]
+                ("isolated_us", C.c_double), ("tmem_columns", C.c_int64), ("cluster_size", C.c_int64)]
 
 
 class OparaSimResult(C.Structure):

@@ -230,6 +230,7 @@ opara_status launch_attention(const opara_op& op, cudaStream_t s, unsigned long 
   c.grid = dim3(static_cast<unsigned>(op.i[1]));
   c.block = dim3(kThreads);
   c.smem = kQBytes + kKBytes + kPBytes + kVBytes + 64 + 1024;
+  c.tmem_cols = 256;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;
   static bool attr = false;

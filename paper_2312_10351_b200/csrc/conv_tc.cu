@@ -1031,6 +1031,7 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
     c.grid = dim3(ceil_div(a.M, 128), 1, 1);
     c.block = dim3(kThreads);
     c.smem = nw == 32 ? tc_px_smem_bytes<32>() : tc_px_smem_bytes<64>();
+    c.tmem_cols = 3 * nw <= 128 ? 128 : 256;
     if (cfg) *cfg = c;
     if (dry) return OPARA_OK;
     static std::mutex mu;
@@ -1083,6 +1084,8 @@ opara_status launch_conv2d_tc(const opara_op& op, cudaStream_t s, unsigned long 
   c.grid = dim3(ceil_div(a.M, v[id].bn), (a.Cout + 127) / 128, a.splits);
   c.block = dim3(kThreads);
   c.smem = v[id].smem + (a.push ? recv_bytes : 0);
+  c.tmem_cols = v[id].bn >= 256 ? 512 : std::max(32, v[id].bn * 4);
+  c.cluster = a.splits;
   c.workspace = a.l2red ? static_cast<size_t>(c.grid.x) * c.grid.y * c.grid.z * v[id].bn * 128 * 4 : 0;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;

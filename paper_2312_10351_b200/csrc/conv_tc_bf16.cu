@@ -1005,6 +1005,8 @@ opara_status launch_conv2d_tc_bf16(const opara_op& op, cudaStream_t s, unsigned 
   c.grid = dim3(ceil_div(a.M, bn), mtiles, a.splits);
   c.block = dim3(kThreads);
   c.smem = v[id].smem + (a.push ? recv_bytes : 0) + r_bytes;
+  c.tmem_cols = bn < 32 ? 32 : bn;
+  c.cluster = a.splits;
   c.workspace = a.l2red ? static_cast<size_t>(c.grid.x) * c.grid.y * c.grid.z * bn * 128 * 4 : 0;
   if (cfg) *cfg = c;
   if (dry) return OPARA_OK;

@@ -393,6 +393,8 @@ opara_status opara_op_launch_config(const opara_op* op, opara_op_profile* out) {
   out->shared_mem_per_block = static_cast<int64_t>(c.smem);
   out->registers_per_thread = 0;
   out->isolated_us = 0.0;
+  out->tmem_columns = c.tmem_cols;
+  out->cluster_size = c.cluster;
   int count = 0;
   if (c.func && cudaGetDeviceCount(&count) == cudaSuccess && count > 0) {
     cudaFuncAttributes attr;
@@ -420,7 +422,7 @@ opara_status opara_exec_profile(opara_exec* ex, int32_t reps, opara_op_profile* 
     st = opara::launch_op(ex->ops[i], s, nullptr, &c, true);
     if (st != OPARA_OK) break;
     if (!c.func) {  // NOP join: no kernel, no demand
-      out[i] = opara_op_profile{1, 0, 0, 0, 0.0};
+      out[i] = opara_op_profile{1, 0, 0, 0, 0.0, 0, 1};
       continue;
     }
     cudaFuncAttributes attr;
@@ -433,6 +435,8 @@ opara_status opara_exec_profile(opara_exec* ex, int32_t reps, opara_op_profile* 
     p.threads_per_block = static_cast<int64_t>(c.block.x) * c.block.y * c.block.z;
     p.shared_mem_per_block = static_cast<int64_t>(c.smem) + static_cast<int64_t>(attr.sharedSizeBytes);
     p.registers_per_thread = attr.numRegs;
+    p.tmem_columns = c.tmem_cols;
+    p.cluster_size = c.cluster;
     // In-graph duration: a graph of `reps` back-to-back launches of this op,
     // replayed three times; the median per-launch time is kept.
     cudaGraph_t g = nullptr;

@@ -54,6 +54,8 @@ struct LaunchCfg {
   dim3 block{1, 1, 1};
   size_t smem = 0;
   size_t workspace = 0;  // private device scratch the executor allocates into op.p[7]
+  int tmem_cols = 0;     // TMEM columns one block allocates (co-residency: 512 per SM)
+  int cluster = 1;       // thread-block cluster size of the launch
 };
 
 // Split-K workspace: `floats` partial values, then one u32 arrival counter per

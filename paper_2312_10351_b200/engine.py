@@ -647,8 +647,19 @@ class ScheduledGraph:
         _lib.check(_lib.lib().opara_exec_profile(self._h, reps, C.cast(out, C.c_void_p)))
         return [dict(num_blocks=p.num_blocks, threads_per_block=p.threads_per_block,
                      shared_mem_per_block=p.shared_mem_per_block,
-                     registers_per_thread=p.registers_per_thread, isolated_us=p.isolated_us)
+                     registers_per_thread=p.registers_per_thread, isolated_us=p.isolated_us,
+                     tmem_columns=p.tmem_columns, cluster_size=p.cluster_size)
                 for p in out]
+
+    def effective_smem(self, p: dict) -> int:
+        """Shared-memory demand Alg. 2 sees.  OPARA_DEMAND=coresident folds the
+        block's TMEM allocation (512 columns per SM) into it, so a kernel whose
+        TMEM share of an SM exceeds its smem share is scored by the scarcer
+        resource (VERDICT r01 #6); default: the measured static + dynamic smem."""
+        smem = p["shared_mem_per_block"]
+        if os.environ.get("OPARA_DEMAND", "") != "coresident" or not p.get("tmem_columns"):
+            return smem
+        return max(smem, -(-p["tmem_columns"] * self.gpu_config.shared_mem_per_sm // 512))
 
     # roofline peaks used by the measured classifier (MEASURED_PEAKS.json values on B200)
     PEAK_TFLOPS = {0: 74.4, 1: 1622.8 / 6, 2: 1622.8}   # SIMT fp32, 3xTF32, bf16 tensor
@@ -672,7 +683,7 @@ class ScheduledGraph:
         measured = self.classify == "measured"
         nodes = []
         for k, (op, p) in enumerate(zip(self.program.ops, self.profile)):
-            d = ResourceDemand(p["threads_per_block"], p["shared_mem_per_block"],
+            d = ResourceDemand(p["threads_per_block"], self.effective_smem(p),
                                p["registers_per_thread"], p["num_blocks"])
             cls = self.measured_class(k) if measured else op.op_class
             nodes.append(OperatorNode(k + 1, op.name, cls, d,
