@@ -53,7 +53,7 @@ __device__ unsigned g_phase_n;
       g_phase[slot][10] = ph[8];                                                                    \
       g_phase[slot][11] = ph[9];                                                                    \
       g_phase[slot][8] = (static_cast<unsigned long long>(a.M) << 40) | (static_cast<unsigned long long>(a.Cout) << 20) | a.K; \
-      g_phase[slot][9] = (static_cast<unsigned long long>(gridDim.x * gridDim.y * gridDim.z) << 32) | (static_cast<unsigned long long>(BN) << 24) | (nkb << 8) | (a.push ? 0x80 : 0) | a.splits; \
+      g_phase[slot][9] = (static_cast<unsigned long long>(gridDim.x * gridDim.y * gridDim.z) << 32) | (static_cast<unsigned long long>(BN) << 24) | (nkb << 8) | (a.push ? 0x80 : 0) | (a.l2red ? 0x40 : 0) | (a.ln_in ? 0x20 : 0) | (a.res_stats ? 0x10 : 0) | a.splits; \
     }                                                                                               \
   } while (0)
 #else
@@ -255,6 +255,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
         piw[j] = 0;
       }
     }
+    // folded-LayerNorm consumers: gamma / beta of this warp's first stage are
+    // parameters — fetched before griddepcontrol.wait, beside the predecessor
+    float4 ln_g0 = make_float4(0.f, 0.f, 0.f, 0.f), ln_g1 = ln_g0, ln_b0 = ln_g0, ln_b1 = ln_g0;
+    if (ln_in && rw < nkb) {
+      const int c0 = (kb0 + rw) * kBK + (lane & 3) * 8;
+      const float4* g4 = reinterpret_cast<const float4*>(a.gb + c0);
+      const float4* b4 = reinterpret_cast<const float4*>(a.gb + a.Cin + c0);
+      ln_g0 = __ldg(g4);
+      ln_g1 = __ldg(g4 + 1);
+      ln_b0 = __ldg(b4);
+      ln_b1 = __ldg(b4 + 1);
+    }
     pdl_wait();
     trace_begin(trace);
     if (tid == 0) PHASE(1);
@@ -319,7 +331,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
           const int c0 = (kb0 + i) * kBK + c4 * 8;   // this lane's 8 channels
           const float4* g4 = reinterpret_cast<const float4*>(a.gb + c0);
           const float4* b4 = reinterpret_cast<const float4*>(a.gb + a.Cin + c0);
-          const float4 ga = __ldg(g4), gb2 = __ldg(g4 + 1), ba = __ldg(b4), bb = __ldg(b4 + 1);
+          const bool first = i == rw;   // prefetched before the PDL wait
+          const float4 ga = first ? ln_g0 : __ldg(g4), gb2 = first ? ln_g1 : __ldg(g4 + 1);
+          const float4 ba = first ? ln_b0 : __ldg(b4), bb = first ? ln_b1 : __ldg(b4 + 1);
           const float g[8] = {ga.x, ga.y, ga.z, ga.w, gb2.x, gb2.y, gb2.z, gb2.w};
           const float b[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
           tc::mbar_wait(&landed[s], (i / kStages) & 1);

@@ -48,7 +48,8 @@ groups = defaultdict(list)
 for r in rec:
     m, cout, k = r[8] >> 40, (r[8] >> 20) & 0xFFFFF, r[8] & 0xFFFFF
     ctas, bn, nkb, flags = r[9] >> 32, (r[9] >> 24) & 0xFF, (r[9] >> 8) & 0xFFFF, r[9] & 0xFF
-    mode = "push" if flags & 0x80 else "glob" if flags & 0x40 else "pull"
+    mode = ("push" if flags & 0x80 else "l2" if flags & 0x40 else "pull") + \
+        (" ln_in" if flags & 0x20 else "") + (" res_stats" if flags & 0x10 else "")
     t = r[:8].copy()
     for q in (5, 6):       # paths without the probe: carry the previous stamp
         if t[q] == 0:
@@ -58,7 +59,7 @@ for r in rec:
         d = np.concatenate([d, [(r[10] - t[4]) / 1e3, (r[11] - r[10]) / 1e3, (t[5] - r[11]) / 1e3]])
     else:
         d = np.concatenate([d, [0, 0, 0]])
-    groups[(int(m), int(cout), int(k), int(ctas), int(bn), int(nkb), int(flags & 0x3F), mode)].append(d)
+    groups[(int(m), int(cout), int(k), int(ctas), int(bn), int(nkb), int(flags & 0x0F), mode)].append(d)
 print(f"{n} launches; phases (us): wait | first stage | mma loop | accum | stage partials | peers ready | "
       "reduce+store || stage: loop | barrier | rest ")
 for key, ds in sorted(groups.items(), key=lambda kv: -len(kv[1])):
