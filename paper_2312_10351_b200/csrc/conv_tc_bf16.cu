@@ -80,8 +80,8 @@ constexpr uint32_t kWBytes = 128 * kBK * 2;  // 8 KB
 // before griddepcontrol.wait (weights do not depend on the predecessor), so
 // after the wait only the small activation tile is on the critical path.
 __host__ __device__ constexpr int bf_stages(int bn) { return bn == 16 ? 24 : bn <= 64 ? 8 : 6; }
-// full[], empty[], accum, tmem slot, push barrier, landed[]: rounded up to 128 bytes
-__host__ __device__ constexpr int bf_bar_bytes(int stages) { return ((3 * stages + 3) * 8 + 127) / 128 * 128; }
+// full[], empty[], accum, tmem slot, push barrier, landed[], LayerNorm stats: rounded up to 128 bytes
+__host__ __device__ constexpr int bf_bar_bytes(int stages) { return ((3 * stages + 4) * 8 + 127) / 128 * 128; }
 
 // kVecBf16: 16-byte cp.async of 8 channels (Cin % 8 == 0); kSub4 / kSub2: each
 // 16-byte smem chunk assembled from 8- / 4-byte cp.asyncs of 4 / 2 channels
@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
   // fp32 behind the ring (other CTAs may push while this CTA's ring is busy)
   uint64_t* rbar = accum + 2;
   uint64_t* landed = rbar + 1;   // TMA tile landed (folded-LayerNorm consumers: normalised before full[])
+  uint64_t* statbar = landed + kStages;   // folded-LayerNorm consumers: per-token mean / rstd in smem
   float* recv = reinterpret_cast<float*>(smem + kStages * kStage + bf_bar_bytes(kStages));
   const bool push = a.push != 0;
   const bool ln_in = kMode == kTma && a.ln_in;
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
       tc::mbar_init(&empty[s], 1);
       if (ln_in) tc::mbar_init(&landed[s], 1);
     }
+    if (ln_in) tc::mbar_init(statbar, 32 * kGatherWarps);
     tc::mbar_init(accum, 1);
     if (push) tc::mbar_init(rbar, 1);
     tc::fence_barrier_init();
@@ -323,7 +325,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
           ln_mean[row] = mu;
           ln_rstd[row] = rsqrtf(fmaxf(s2 / a.Cin - mu * mu, 0.f) + a.eps);
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kGatherWarps) : "memory");   // the gather warps only
+        // every gather thread has published its rows' statistics (an mbarrier
+        // among the gather warps only; the other warps never wait on it)
+        tc::mbar_arrive(statbar);
+        tc::mbar_wait(statbar, 0);
         const int c4 = lane & 3, rl = lane >> 2;
         const bool write = a.lnout && mt == 0;
         for (int i = rw; i < nkb; i += kGatherWarps) {
