@@ -184,3 +184,37 @@ def test_deepfm_lowering_shape():
     last = prog.ops[-1]
     assert last.kind == frontend.ADD and last.ints["n"] == 3 and last.ints["act"] == frontend.ACT_SIGMOID
     assert len(prog.inputs) == 2 and prog.inputs[1].dtype == "i64"
+
+
+def test_bert_layernorm_folding_lowering():
+    """bf16 BERT: 23 of 24 add_layer_norms fold into the GEMMs around them
+    (frontend.PendingLN); the output LayerNorm stays a kernel.  Producers get
+    the residual as a second input and the stats tensor as an extra output;
+    every consumer reads (o, stats, residual); exactly one consumer per folded
+    LayerNorm writes the normalised rows, before any GEMM reads them as a
+    residual; fold_ln=False keeps every LayerNorm kernel."""
+    m, _, ids = zoo.build_bert()
+    prog = frontend.lower(m, ids, "bf16")
+    ops = prog.ops
+    assert sum(1 for o in ops if o.kind == frontend.LAYERNORM) == 1
+    prods = [k for k, o in enumerate(ops) if o.ints.get("res_stats")]
+    cons = [k for k, o in enumerate(ops) if o.ints.get("ln_in")]
+    writers = [k for k in cons if ops[k].ints.get("ln_write")]
+    assert (len(prods), len(writers), len(cons)) == (23, 23, 23 + 11 * 2)
+    edges = set(prog.edges)
+    for k in prods:
+        o = ops[k]
+        assert len(o.inputs) == 2 and len(o.extra_outputs) == 1 and o.ints.get("act", 0) == 0
+        assert o.extra_outputs[0].producers == {k} and o.extra_outputs[0].shape == (128, 12)
+    for k in cons:
+        o = ops[k]
+        assert len(o.inputs) == 3 and o.ints["ln_tiles"] == 6 and o.arrays["gb"].shape == (2, 768)
+        producer = min(o.inputs[1].producers)
+        assert ops[producer].ints.get("res_stats") and (producer, k) in edges
+    for k in writers:   # the normalised rows exist before any GEMM reads them as its residual
+        out = ops[k].extra_outputs[0]
+        readers = [j for j, o in enumerate(ops) if any(t is out for t in o.inputs)]
+        assert readers and all(j > k and (k, j) in edges for j in readers)
+    unfolded = frontend.lower(m, ids, "bf16", fold_ln=False)
+    assert sum(1 for o in unfolded.ops if o.kind == frontend.LAYERNORM) == 24
+    assert not any(o.ints.get("ln_in") or o.ints.get("res_stats") for o in unfolded.ops)
