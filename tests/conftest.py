@@ -3,7 +3,9 @@
 from __future__ import annotations
 
 import json
+import os
 import sys
+import tempfile
 from functools import lru_cache
 from pathlib import Path
 
@@ -18,6 +20,13 @@ GOLDEN = ROOT / "tests" / "golden"
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
     config.addinivalue_line("markers", "slow: longer CPU-only cases")
+    # One tile-tuning cache per test session: the GPU suite compiles the same
+    # models many times (per split-K mode, grid policy and bench variant), and
+    # every (shape, budget, reduction) key is tuned once instead of per compile.
+    # Any cached choice is a measured-valid tile; tests that need a private
+    # cache set their own (monkeypatch).
+    if "OPARA_TUNE_CACHE" not in os.environ:
+        os.environ["OPARA_TUNE_CACHE"] = os.path.join(tempfile.mkdtemp(prefix="opara_tune_"), "tune.json")
 
 
 def pytest_collection_modifyitems(config, items):
