@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_tf32x3(const __grid_con
         const int w0 = ow * a.sw - a.pw, h0 = oh * a.sh - a.ph;
         const int kc = kb0 * kBKF, rs = kc / a.Cin;
         int dc = kc - rs * a.Cin, dr = rs / a.S, dq = rs - dr * a.S;
+        tc::prefetch_tmap(&a.tmap);
         pdl_wait();
         trace_begin(trace);
         for (int i = 0; i < nkb; ++i) {

@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
       ln_b0 = __ldg(b4);
       ln_b1 = __ldg(b4 + 1);
     }
+    if (kMode == kTma && tid == 0 && !ln_in) tc::prefetch_tmap(&a.tmap);
     pdl_wait();
     trace_begin(trace);
     if (tid == 0) PHASE(1);
@@ -547,6 +548,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv2d_tc_bf16(const __grid_const
     if (ln_in && lane == 0) {
       // folded-LayerNorm consumers: each stage's o and r tiles land on
       // landed[]; the gather warps normalise them before releasing full[]
+      tc::prefetch_tmap(&a.tmap);
+      tc::prefetch_tmap(&a.tmap_r);
       pdl_wait();
       const int kc = kb0 * kBK;
       for (int i = 0; i < nkb; ++i) {

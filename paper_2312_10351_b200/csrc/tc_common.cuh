@@ -97,6 +97,12 @@ __device__ __forceinline__ void tma_im2col_4d(void* dst, const void* tmap, int c
       : "memory");
 }
 
+// Pull a tensor map (a __grid_constant__ kernel parameter) into the TMA
+// descriptor cache ahead of its first use (issued before griddepcontrol.wait).
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05
 
 // Allocate `ncols` TMEM columns (power of two >= 32); one full warp calls it.
