@@ -4,11 +4,11 @@
 //   O = P V / rowsum   (tcgen05.mma, M = 128 queries, N = 64, K = 128 keys)
 // Q, K, V and O are channel views of [tokens][C] bf16 buffers (head h reads
 // columns off + h*64 ..); S and O accumulate in TMEM (fp32).  Every operand
-// is staged by cp.async straight from its natural row layout: Q, K as
-// 64-byte-swizzled K-major atoms, V as an MN-major operand (8-key x 32-d
-// atoms, MN atoms 512 B apart, key groups 1024 B apart; probed in
-// scripts/micro/umma_mn.cu), so no transpose pass; P is written by the
-// softmax warps.  Softmax: the four warps w, w+4, w+8, w+12 share TMEM lane
+// lands by TMA (2-D tiled maps, 32-column x 128-row boxes, 64-byte swizzle)
+// straight from its natural row layout: Q, K as K-major atoms, V as an
+// MN-major operand (8-key x 32-d atoms; descriptor LBO = MN atom stride, SBO =
+// 8-key group stride, probed in scripts/micro/umma_mn.cu), so no transpose
+// pass; P is written by the softmax warps.  Softmax: the four warps w, w+4, w+8, w+12 share TMEM lane
 // quarter w % 4 (query rows 32(w%4)..) and split the 128 keys in quarters;
 // row max and row sum are combined through shared memory.  Shapes: tokens =
 // 128, head_dim = 64 (BERT-base, seq 128).
@@ -19,6 +19,7 @@
 #include "ops.h"
 #include "status.h"
 #include "tc_common.cuh"
+#include "tma_host.h"
 
 namespace opara {
 namespace {
@@ -27,6 +28,7 @@ constexpr int kT = 128, kD = 64, kThreads = 512, kWarps = kThreads / 32;
 constexpr uint32_t kQBytes = kT * kD * 2, kKBytes = kT * kD * 2, kPBytes = kT * kT * 2, kVBytes = kD * kT * 2;
 
 struct AttnArgs {
+  CUtensorMap tq, tk, tv;   // 2-D tiled maps of the Q, K, V buffers: 32-column x 128-row boxes, SW64
   const __nv_bfloat16* q;
   const __nv_bfloat16* k;
   const __nv_bfloat16* v;
@@ -44,12 +46,9 @@ __device__ __forceinline__ uint32_t sw64(int rows, int row, int c16) {
   return static_cast<uint32_t>(kb * rows * 64 + (row >> 3) * 512 + r8 * 64 + ((cw ^ ((r8 >> 1) & 3)) << 4));
 }
 
-// MN-major SW64 V operand: chunk c16 (d = 8 c16 ..) of key row `key`.
-constexpr uint32_t kVLbo = 512, kVSbo = 1024;   // MN atom stride, 8-key group stride
-__device__ __forceinline__ uint32_t vmn(int key, int c16) {
-  const int r = key & 7;
-  return static_cast<uint32_t>((c16 >> 2) * kVLbo + (key >> 3) * kVSbo + r * 64 + (((c16 & 3) ^ ((r >> 1) & 3)) << 4));
-}
+// MN-major SW64 V operand as two TMA boxes of 32 head dims x 128 keys: key
+// row = 64 B, 8-key atoms 512 B apart along K, the second 32 dims 8 KB on.
+constexpr uint32_t kVLbo = kT * 64, kVSbo = 512;   // MN atom stride, 8-key group stride
 
 __device__ __forceinline__ uint64_t desc_mn_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -61,28 +60,27 @@ __device__ __forceinline__ uint64_t desc_mn_sw64(uint32_t saddr, uint32_t lbo, u
   return d;
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-
-__global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned long long* trace) {
+__global__ void __launch_bounds__(kThreads, 1) attention_tc(const __grid_constant__ AttnArgs a,
+                                                             unsigned long long* trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* qs = smem;
   uint8_t* ks = qs + kQBytes;
   uint8_t* ps = ks + kKBytes;
   uint8_t* vs = ps + kPBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(vs + kVBytes);  // [0] S ready, [1] O ready
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vs + kVBytes);  // [0] S ready, [1] O ready, [2] Q+K, [3] V landed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
   __shared__ float red_max[4][kT], red_sum[4][kT];
 
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = blockIdx.x;
   if (tid == 0) {
-    tc::mbar_init(&bar[0], 1);
-    tc::mbar_init(&bar[1], 1);
+    for (int b = 0; b < 4; ++b) tc::mbar_init(&bar[b], 1);
     tc::fence_barrier_init();
+    tc::prefetch_tmap(&a.tq);
+    tc::prefetch_tmap(&a.tk);
+    tc::prefetch_tmap(&a.tv);
   }
   if (warp == 0) tc::tmem_alloc(tslot, 256);
   tc::tc_fence_before();
@@ -93,34 +91,22 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
 
   pdl_wait();
   trace_begin(trace);
-  // ---- stage Q, K (K-major) and V (MN-major): 3 x 1024 16-byte chunks, every
-  // copy in flight at once; S = Q K^T is issued once Q and K have landed,
-  // while V's group is still on the way
-  const __nv_bfloat16* qg = a.q + a.q_off + h * kD;
-  const __nv_bfloat16* kg = a.k + a.k_off + h * kD;
-  const __nv_bfloat16* vg = a.v + a.v_off + h * kD;
-  constexpr int kChunks = kT * (kD / 8) / kThreads;   // 16-byte chunks per thread per operand
-#pragma unroll
-  for (int j = 0; j < kChunks; ++j) {
-    const int u = tid + j * kThreads, row = u >> 3, c16 = u & 7;
-    cp_async16(tc::smem_u32(qs) + sw64(kT, row, c16), qg + static_cast<int64_t>(row) * a.q_stride + c16 * 8);
-    cp_async16(tc::smem_u32(ks) + sw64(kT, row, c16), kg + static_cast<int64_t>(row) * a.k_stride + c16 * 8);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-#pragma unroll
-  for (int j = 0; j < kChunks; ++j) {
-    const int u = tid + j * kThreads, key = u >> 3, c16 = u & 7;
-    cp_async16(tc::smem_u32(vs) + vmn(key, c16), vg + static_cast<int64_t>(key) * a.v_stride + c16 * 8);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 1;" ::: "memory");
-  tc::fence_proxy_async_smem();
-  __syncthreads();
-
-  // ---- S = Q K^T
+  // ---- Q, K (K-major: two 32-column boxes each) and V (MN-major: two 32-dim
+  // boxes) land by TMA; S = Q K^T is issued once Q and K have landed, while V
+  // is still on the way
   constexpr uint32_t kIdS = tc::instr_desc(1, 128, 128);
   constexpr uint32_t kIdO = tc::instr_desc(1, 128, 64) | (1u << 16);   // B (V) MN-major
   if (tid == 0) {
+    const int qc = a.q_off + h * kD, kc = a.k_off + h * kD, vc = a.v_off + h * kD;
+    tc::mbar_arrive_expect_tx(&bar[2], kQBytes + kKBytes);
+    tc::tma_tile_2d(qs, &a.tq, qc, 0, &bar[2]);
+    tc::tma_tile_2d(qs + kT * 64, &a.tq, qc + 32, 0, &bar[2]);
+    tc::tma_tile_2d(ks, &a.tk, kc, 0, &bar[2]);
+    tc::tma_tile_2d(ks + kT * 64, &a.tk, kc + 32, 0, &bar[2]);
+    tc::mbar_arrive_expect_tx(&bar[3], kVBytes);
+    tc::tma_tile_2d(vs, &a.tv, vc, 0, &bar[3]);
+    tc::tma_tile_2d(vs + kVLbo, &a.tv, vc + 32, 0, &bar[3]);
+    tc::mbar_wait(&bar[2], 0);
     tc::tc_fence_after();
 #pragma unroll
     for (int s = 0; s < kD / 16; ++s) {
@@ -130,8 +116,6 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
     }
     tc::mma_commit(&bar[0]);
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");   // V landed (this thread's chunks)
-  tc::fence_proxy_async_smem();
   tc::mbar_wait(&bar[0], 0);
   tc::tc_fence_after();
 
@@ -177,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) attention_tc(AttnArgs a, unsigned
 
   // ---- O = P V
   if (tid == 0) {
+    tc::mbar_wait(&bar[3], 0);   // V landed
     tc::tc_fence_after();
 #pragma unroll
     for (int s = 0; s < kT / 16; ++s) {
@@ -239,6 +224,10 @@ opara_status launch_attention(const opara_op& op, cudaStream_t s, unsigned long 
     if (e != cudaSuccess) return cuda_fail(e, "attention_tc smem attribute");
     attr = true;
   }
+  if (!make_tiled_bf16_map(&a.tq, a.q, a.q_stride, kT, 32, kT) ||
+      !make_tiled_bf16_map(&a.tk, a.k, a.k_stride, kT, 32, kT) ||
+      !make_tiled_bf16_map(&a.tv, a.v, a.v_stride, kT, 32, kT))
+    return fail(OPARA_ERR_CUDA, "attention_tc: cuTensorMapEncodeTiled failed");
   void* args[] = {&a, &trace};
   return launch_kernel(c, args, s);
 }

@@ -97,6 +97,14 @@ __device__ __forceinline__ void tma_im2col_4d(void* dst, const void* tmap, int c
       : "memory");
 }
 
+// TMA tiled 2-D load of one box at element coordinates (c0, c1) into `dst`.
+__device__ __forceinline__ void tma_tile_2d(void* dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Pull a tensor map (a __grid_constant__ kernel parameter) into the TMA
 // descriptor cache ahead of its first use (issued before griddepcontrol.wait).
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
